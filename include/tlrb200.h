@@ -1,0 +1,120 @@
+/*
+ * tlrb200.h — C ABI of the B200-native TLR Gaussian log-likelihood library
+ * (libtlrb200.so).  Plain pointers and sizes only; no torch / CUDA types.
+ *
+ * The drop-in boundary replaces these reference entry points
+ * (/root/reference/pkg/src/tlrgeo/):
+ *   stats.log_likelihood        stats.py:103-112   -> tlrb_loglik
+ *   stats._factorize            stats.py:96-100    -> (inside tlrb_loglik)
+ *   tilestore.assemble_covariance tilestore.py:181-223 -> (inside tlrb_loglik)
+ *   linalg.cholesky / tlr_cholesky / dense_cholesky linalg.py:82-147
+ *   linalg.quadratic_form       linalg.py:200-206
+ *   linalg.solve_cholesky       linalg.py:195-197  -> tlrb_solve
+ *   predict.predict (mean)      predict.py:65-87   -> tlrb_predict
+ *   kernels.bessel_k            kernels.py:216-226 -> tlrb_bessel_k
+ *   kernels.matern_block        kernels.py:494-530 -> tlrb_matern_block
+ *   compression.compress_tile   compression.py:39-51 -> tlrb_compress_tile
+ *   linalg.NotPositiveDefiniteError linalg.py:20-33 -> TLRB_ERR_NPD + tlrb_last_error
+ *
+ * Return codes of every int-returning call.
+ */
+#ifndef TLRB200_H
+#define TLRB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLRB_OK 0
+#define TLRB_ERR_NPD 1     /* not positive definite: (tile, pivot) via tlrb_last_error */
+#define TLRB_ERR_ARG 2     /* invalid argument (shape, theta, accuracy) */
+#define TLRB_ERR_CUDA 3    /* CUDA / NCCL / out-of-memory */
+
+typedef struct tlrb_handle tlrb_handle;
+
+/* Per-evaluation statistics (phase times measured with CUDA events on the
+ * handle's stream; algorithmic work counted from the actual ranks). */
+typedef struct tlrb_stats {
+  double ms_generate;     /* tile generation (+ initial compression in TLR) */
+  double ms_compress;     /* initial compression only */
+  double ms_factor;       /* tile Cholesky */
+  double ms_solve;        /* forward solve + dot + log-det reduction */
+  double ms_total;
+  double flops;           /* algorithmic FP64 flops (SURVEY 8(d) formulas) */
+  double bytes;           /* algorithmic HBM bytes (SURVEY 8(d) formulas) */
+  int64_t stored_reals;   /* footprint() semantics, tilestore.py:150-163 */
+  int64_t kernel_launches;/* kernels launched by this call */
+  int32_t max_rank;       /* of the final factor's off-diagonal tiles */
+  double mean_rank;
+  int32_t sketch_retries; /* compression sketches that had to be enlarged */
+  int32_t jacobi_max_sweeps;
+} tlrb_stats;
+
+/* Create a handle for n locations (xy: n x 2, row-major, like
+ * LocationSet.coords).  nb: tile size (min(nb, n) is used), ngpus: 1 in this
+ * build, max_rank: <=0 means uncapped, device: CUDA ordinal.  Locations stay
+ * resident on the device across evaluations.  *err receives a TLRB_* code. */
+tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
+                         int32_t max_rank, int32_t device, int32_t* err);
+void tlrb_destroy(tlrb_handle* h);
+
+/* One Gaussian log-likelihood evaluation
+ *   ll = -0.5 (n log 2pi + log|Sigma| + z' Sigma^-1 z)     (stats.py:112)
+ * z: host pointer (n doubles).  acc == 0 -> dense mode, else TLR(acc).
+ * Any of ll/logdet/quad/st may be NULL. */
+int32_t tlrb_loglik(tlrb_handle* h, const double* z, double theta1, double theta2,
+                    double theta3, double nugget, double acc, double* ll,
+                    double* logdet, double* quad, tlrb_stats* st);
+
+/* Same, with z already resident in device memory (used for the HBM-resident
+ * throughput measurement). */
+int32_t tlrb_loglik_device(tlrb_handle* h, const double* d_z, double theta1,
+                           double theta2, double theta3, double nugget, double acc,
+                           double* ll, double* logdet, double* quad, tlrb_stats* st);
+
+/* Solve Sigma x = rhs with the factor of the last successful tlrb_loglik /
+ * tlrb_predict call (linalg.solve_cholesky semantics).  rhs, x: host, n. */
+int32_t tlrb_solve(tlrb_handle* h, const double* rhs, double* x);
+
+/* Kriging mean (predict.py:65-87): factorize Sigma_22 over the handle's
+ * locations, w = Sigma_22^-1 z, pred = Sigma_12 w with Sigma_12 generated on
+ * the fly (never materialised).  xy_unknown: m x 2 row-major host array. */
+int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown,
+                     int64_t m, double theta1, double theta2, double theta3,
+                     double nugget, double acc, double* pred);
+
+/* Tile rank map of the last factor: ranks[i*t + j] for i > j (t = tiles);
+ * -1 marks a tile stored dense.  Returns t via *t_out. */
+int32_t tlrb_rank_map(tlrb_handle* h, int32_t* ranks, int32_t cap, int32_t* t_out);
+
+/* Last error of the handle: NPD tile / pivot (linalg.py:43-44) and message. */
+int32_t tlrb_last_error(tlrb_handle* h, int32_t* tile, int32_t* pivot, char* msg,
+                        int32_t len);
+
+/* ---- stand-alone device kernels, for parity tests of single components ---- */
+
+/* out[i] = K_nu(x[i]) on the device (kernels.py:160-174). */
+int32_t tlrb_bessel_k(double nu, const double* x, int64_t count, double* out,
+                      int32_t device);
+
+/* out (m x n, column-major, ld = m) = Matern block between row points and
+ * column points (kernels.py:494-530, no nugget). */
+int32_t tlrb_matern_block(const double* rows_xy, int64_t m, const double* cols_xy,
+                          int64_t n, double theta1, double theta2, double theta3,
+                          double* out, int32_t device);
+
+/* Compress one dense m x n tile (column-major) to relative Frobenius accuracy
+ * acc with the device compressor (compression.py:39-51).  u: m x k, v: n x k
+ * (column-major, ld = m / n; caller provides min(m,n) columns). */
+int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc,
+                           int32_t* rank, double* u, double* v, int32_t device);
+
+/* Number of kernels this library has launched in this process. */
+int64_t tlrb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

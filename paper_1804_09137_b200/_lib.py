@@ -1,0 +1,89 @@
+"""ctypes binding of libtlrb200.so (the C ABI declared in include/tlrb200.h).
+
+The product path has no CPU fallback: if the shared library is missing or
+fails to load, every entry point raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libtlrb200.so"
+
+TLRB_OK, TLRB_ERR_NPD, TLRB_ERR_ARG, TLRB_ERR_CUDA = 0, 1, 2, 3
+
+
+class TlrbStats(C.Structure):
+    _fields_ = [
+        ("ms_generate", C.c_double),
+        ("ms_compress", C.c_double),
+        ("ms_factor", C.c_double),
+        ("ms_solve", C.c_double),
+        ("ms_total", C.c_double),
+        ("flops", C.c_double),
+        ("bytes", C.c_double),
+        ("stored_reals", C.c_int64),
+        ("kernel_launches", C.c_int64),
+        ("max_rank", C.c_int32),
+        ("mean_rank", C.c_double),
+        ("sketch_retries", C.c_int32),
+        ("jacobi_max_sweeps", C.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+# (name, restype, argtypes) — mirrors include/tlrb200.h
+_DP = C.POINTER(C.c_double)
+_IP = C.POINTER(C.c_int32)
+SIGNATURES = [
+    ("tlrb_create", C.c_void_p, [_DP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _IP]),
+    ("tlrb_destroy", None, [C.c_void_p]),
+    ("tlrb_loglik", C.c_int32, [C.c_void_p, _DP, C.c_double, C.c_double, C.c_double, C.c_double,
+                                C.c_double, _DP, _DP, _DP, C.POINTER(TlrbStats)]),
+    ("tlrb_loglik_device", C.c_int32, [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_double, _DP, _DP, _DP, C.POINTER(TlrbStats)]),
+    ("tlrb_solve", C.c_int32, [C.c_void_p, _DP, _DP]),
+    ("tlrb_predict", C.c_int32, [C.c_void_p, _DP, _DP, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                 C.c_double, C.c_double, _DP]),
+    ("tlrb_rank_map", C.c_int32, [C.c_void_p, _IP, C.c_int32, _IP]),
+    ("tlrb_last_error", C.c_int32, [C.c_void_p, _IP, _IP, C.c_char_p, C.c_int32]),
+    ("tlrb_bessel_k", C.c_int32, [C.c_double, _DP, C.c_int64, _DP, C.c_int32]),
+    ("tlrb_matern_block", C.c_int32, [_DP, C.c_int64, _DP, C.c_int64, C.c_double, C.c_double,
+                                      C.c_double, _DP, C.c_int32]),
+    ("tlrb_compress_tile", C.c_int32, [_DP, C.c_int32, C.c_int32, C.c_double, _IP, _DP, _DP, C.c_int32]),
+    ("tlrb_launch_count", C.c_int64, []),
+]
+
+
+def load():
+    """Load libtlrb200.so (raises if it is absent: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("TLRB200_LIB", LIB_PATH))
+    if not path.exists():
+        raise RuntimeError(f"libtlrb200.so not found at {path}; run __graft_entry__.build() "
+                           "(the B200 path has no CPU fallback)")
+    lib = C.CDLL(str(path))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+def iptr(a: np.ndarray):
+    return a.ctypes.data_as(_IP)

@@ -1,0 +1,369 @@
+"""Drop-in Python surface for the reference's likelihood / kriging path.
+
+Mirrors (names, argument meaning, error behaviour) the reference package
+`tlrgeo` (/root/reference/pkg/src/tlrgeo):
+
+  MaternParams          kernels.py:34-65
+  LocationSet           geometry.py:78-149 (Euclidean metric)
+  generate_locations    geometry.py:186-206
+  LikelihoodConfig      stats.py:41-70   (+ max_rank, ngpus)
+  log_likelihood        stats.py:103-112
+  PredictionProblem     predict.py:20-48
+  predict (mean)        predict.py:65-87
+  NotPositiveDefiniteError linalg.py:20-33
+  bessel_k, matern_block, compress_tile (component entry points)
+
+Every numerical call goes through libtlrb200.so (hand-written sm_100a CUDA);
+nothing here computes on the CPU beyond argument marshalling.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import TlrbStats, dptr, iptr
+
+THETA3_MAX = 5.0
+DEFAULT_NB_DENSE = 200          # tilestore.py:19
+DEFAULT_NB_TLR = 400            # tilestore.py:20
+LOG_2PI = math.log(2.0 * math.pi)
+
+
+class NotPositiveDefiniteError(Exception):
+    """Same contract as the reference (linalg.py:20-33)."""
+
+    def __init__(self, tile_index: int, pivot_index: int):
+        self.tile_index = tile_index
+        self.pivot_index = pivot_index
+        super().__init__(
+            f"covariance not positive definite at tile {tile_index}, "
+            f"pivot {pivot_index}; consider adding a nugget")
+
+
+class DeviceError(RuntimeError):
+    """CUDA / out-of-memory failure inside libtlrb200.so."""
+
+
+@dataclass(frozen=True)
+class MaternParams:
+    """(variance, range, smoothness) + nugget; validation of kernels.py:43-57."""
+
+    theta1: float
+    theta2: float
+    theta3: float
+    nugget: float = 0.0
+
+    def __post_init__(self):
+        vals = (self.theta1, self.theta2, self.theta3, self.nugget)
+        if not all(math.isfinite(v) for v in vals):
+            raise ValueError(f"non-finite Matern parameters: {vals}")
+        if self.theta1 <= 0 or self.theta2 <= 0 or self.theta3 <= 0:
+            raise ValueError(f"theta components must be strictly positive, got "
+                             f"({self.theta1}, {self.theta2}, {self.theta3})")
+        if self.theta3 > THETA3_MAX:
+            raise ValueError(f"smoothness theta3={self.theta3} exceeds supported bound {THETA3_MAX}")
+        if self.nugget < 0:
+            raise ValueError(f"nugget must be non-negative, got {self.nugget}")
+
+    @property
+    def prefactor(self) -> float:
+        return self.theta1 / (2.0 ** (self.theta3 - 1.0) * math.gamma(self.theta3))
+
+    def as_tuple(self):
+        return (self.theta1, self.theta2, self.theta3, self.nugget)
+
+
+class LocationSet:
+    """Ordered set of distinct unit-square (Euclidean) locations, (n, 2)."""
+
+    def __init__(self, coords, metric=None):
+        coords = np.ascontiguousarray(coords, dtype=float)
+        if coords.ndim != 2 or coords.shape[1] != 2 or coords.shape[0] == 0:
+            raise ValueError(f"coords must be a non-empty (n, 2) array, got {coords.shape}")
+        if not np.isfinite(coords).all():
+            raise ValueError("locations must be finite")
+        if metric is not None and type(metric).__name__ != "Euclidean":
+            raise ValueError("only the Euclidean metric is on the B200 path")
+        if np.unique(coords, axis=0).shape[0] != coords.shape[0]:
+            raise ValueError("locations must be pairwise distinct")
+        coords.setflags(write=False)
+        self.coords = coords
+        self.metric = metric
+
+    def __len__(self) -> int:
+        return self.coords.shape[0]
+
+
+def generate_locations(n: int, seed: int) -> LocationSet:
+    """Jittered ceil(sqrt n) grid in [0,1]^2, row-major (geometry.py:186-206)."""
+    if n < 1:
+        raise ValueError(f"n must be >= 1, got {n}")
+    g = math.isqrt(n)
+    if g * g < n:
+        g += 1
+    off = np.random.default_rng(seed).uniform(-0.4, 0.4, (n, 2))
+    idx = np.arange(n)
+    coords = np.column_stack(((idx // g + 0.5 + off[:, 0]) / g,
+                              (idx % g + 0.5 + off[:, 1]) / g))
+    return LocationSet(coords)
+
+
+@dataclass(frozen=True)
+class LikelihoodConfig:
+    """stats.py:41-70 fields used by the likelihood, plus the build's
+    `max_rank` (tile storage cap; <=0/None = uncapped) and `ngpus`."""
+
+    mode: str = "dense"
+    accuracy: float | None = None
+    nb: int | None = None
+    nugget: float = 0.0
+    bounds: tuple = ((0.01, 5.0), (0.001, 3.0), (0.1, 3.0))
+    theta0: tuple | None = None
+    max_iterations: int = 100
+    tol: float = 1e-9
+    profile: object = "auto"
+    max_rank: int | None = None
+    ngpus: int = 1
+
+    def __post_init__(self):
+        if self.mode not in ("dense", "tlr"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.mode == "tlr" and self.accuracy is None:
+            raise ValueError("tlr mode requires an accuracy threshold")
+        if self.mode == "tlr" and not (0.0 < self.accuracy < 1.0):
+            raise ValueError(f"accuracy must lie in (0, 1), got {self.accuracy}")
+
+    def tile_size(self) -> int:
+        if self.nb is not None:
+            return self.nb
+        return DEFAULT_NB_DENSE if self.mode == "dense" else DEFAULT_NB_TLR
+
+
+# --------------------------------------------------------------------------
+class Handle:
+    """Owns one libtlrb200 handle: locations resident on the device, tile
+    arenas reused across evaluations (one MLE run = one handle)."""
+
+    def __init__(self, coords: np.ndarray, nb: int, max_rank: int = 0, ngpus: int = 1,
+                 device: int = 0):
+        self.lib = _lib.load()
+        xy = np.ascontiguousarray(coords, dtype=np.float64)
+        self.n = xy.shape[0]
+        self.nb = int(min(nb, self.n))
+        err = np.zeros(1, np.int32)
+        self.h = self.lib.tlrb_create(dptr(xy), self.n, self.nb, int(ngpus), int(max_rank or 0),
+                                      int(device), iptr(err))
+        if not self.h:
+            raise (ValueError if err[0] == _lib.TLRB_ERR_ARG else DeviceError)(
+                f"tlrb_create failed (code {int(err[0])})")
+        self.last_stats: dict | None = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tlrb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, rc: int):
+        tile = np.zeros(1, np.int32)
+        piv = np.zeros(1, np.int32)
+        buf = C.create_string_buffer(512)
+        self.lib.tlrb_last_error(self.h, iptr(tile), iptr(piv), buf, 512)
+        if rc == _lib.TLRB_ERR_NPD:
+            raise NotPositiveDefiniteError(int(tile[0]), int(piv[0]))
+        if rc == _lib.TLRB_ERR_ARG:
+            raise ValueError(buf.value.decode() or "invalid argument")
+        raise DeviceError(buf.value.decode() or f"libtlrb200 error {rc}")
+
+    def loglik(self, z: np.ndarray, p: MaternParams, acc: float | None):
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        out = np.zeros(3)
+        st = TlrbStats()
+        rc = self.lib.tlrb_loglik(self.h, dptr(z), p.theta1, p.theta2, p.theta3, p.nugget,
+                                  float(acc or 0.0), dptr(out[0:]), dptr(out[1:]), dptr(out[2:]),
+                                  C.byref(st))
+        if rc:
+            self._raise(rc)
+        self.last_stats = st.as_dict()
+        return float(out[0]), float(out[1]), float(out[2])
+
+    def loglik_device(self, z_ptr: int, p: MaternParams, acc: float | None):
+        out = np.zeros(3)
+        st = TlrbStats()
+        rc = self.lib.tlrb_loglik_device(self.h, C.c_void_p(z_ptr), p.theta1, p.theta2, p.theta3,
+                                         p.nugget, float(acc or 0.0), dptr(out[0:]), dptr(out[1:]),
+                                         dptr(out[2:]), C.byref(st))
+        if rc:
+            self._raise(rc)
+        self.last_stats = st.as_dict()
+        return float(out[0]), float(out[1]), float(out[2])
+
+    def solve(self, rhs: np.ndarray) -> np.ndarray:
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty_like(rhs)
+        rc = self.lib.tlrb_solve(self.h, dptr(rhs), dptr(x))
+        if rc:
+            self._raise(rc)
+        return x
+
+    def predict(self, z, unknown_xy, p: MaternParams, acc: float | None) -> np.ndarray:
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        u = np.ascontiguousarray(unknown_xy, dtype=np.float64)
+        out = np.empty(u.shape[0])
+        rc = self.lib.tlrb_predict(self.h, dptr(z), dptr(u), u.shape[0], p.theta1, p.theta2,
+                                   p.theta3, p.nugget, float(acc or 0.0), dptr(out))
+        if rc:
+            self._raise(rc)
+        return out
+
+    def rank_map(self) -> np.ndarray:
+        t = np.zeros(1, np.int32)
+        self.lib.tlrb_rank_map(self.h, None, 0, iptr(t))
+        tt = int(t[0])
+        r = np.zeros(tt * tt, np.int32)
+        self.lib.tlrb_rank_map(self.h, iptr(r), tt * tt, iptr(t))
+        return r.reshape(tt, tt)
+
+
+_HANDLES: dict = {}
+
+
+def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus) -> Handle:
+    key = (coords.__array_interface__["data"][0], coords.shape[0], int(nb), int(max_rank or 0), ngpus)
+    h = _HANDLES.get(key)
+    if h is None or h[0] is not coords:
+        if len(_HANDLES) > 8:
+            _HANDLES.clear()
+        h = (coords, Handle(coords, nb, max_rank or 0, ngpus))
+        _HANDLES[key] = h
+    return h[1]
+
+
+def _coords_of(locs) -> np.ndarray:
+    coords = getattr(locs, "coords", None)
+    if coords is None:
+        raise TypeError("locs must be a LocationSet (with .coords)")
+    return coords
+
+
+def log_likelihood(locs, z, p: MaternParams, cfg: LikelihoodConfig = LikelihoodConfig()) -> float:
+    """Gaussian log-likelihood of z under Sigma(p); one device factorization.
+
+    Same signature / errors as tlrgeo.stats.log_likelihood (stats.py:103-112).
+    """
+    z = np.asarray(z, dtype=float)
+    n = len(locs)
+    if z.shape != (n,):
+        raise ValueError(f"measurement vector shape {z.shape} does not match n={n}")
+    coords = _coords_of(locs)
+    nb = min(cfg.tile_size(), n)
+    h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus)
+    acc = cfg.accuracy if cfg.mode == "tlr" else None
+    ll, _, _ = h.loglik(z, p, acc)
+    return ll
+
+
+def log_likelihood_parts(locs, z, p: MaternParams, cfg: LikelihoodConfig = LikelihoodConfig()):
+    """(ll, log_det, quad, stats) — diagnostic variant of log_likelihood."""
+    z = np.asarray(z, dtype=float)
+    coords = _coords_of(locs)
+    nb = min(cfg.tile_size(), len(locs))
+    h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus)
+    ll, ld, q = h.loglik(z, p, cfg.accuracy if cfg.mode == "tlr" else None)
+    return ll, ld, q, h.last_stats
+
+
+@dataclass(frozen=True)
+class PredictionProblem:
+    """predict.py:20-48."""
+
+    known: object
+    z: np.ndarray
+    unknown: object
+    theta: MaternParams
+    mode: str = "dense"
+    accuracy: float | None = None
+    nb: int | None = None
+    max_rank: int | None = None
+
+    def __post_init__(self):
+        z = np.asarray(self.z, dtype=float)
+        if z.shape != (len(self.known),):
+            raise ValueError(f"measurement shape {z.shape} does not match {len(self.known)} locations")
+        if self.mode not in ("dense", "tlr"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.mode == "tlr" and self.accuracy is None:
+            raise ValueError("tlr mode requires an accuracy threshold")
+
+    def tile_size(self) -> int:
+        if self.nb is not None:
+            return self.nb
+        return DEFAULT_NB_DENSE if self.mode == "dense" else DEFAULT_NB_TLR
+
+
+def predict(p: PredictionProblem, with_variance: bool = False):
+    """Kriging mean Sigma_12 Sigma_22^-1 z (predict.py:65-87).  The
+    conditional-variance branch is not on the B200 path yet."""
+    if with_variance:
+        raise NotImplementedError("conditional variance is not on the B200 path (SURVEY 8(f) f3)")
+    coords = _coords_of(p.known)
+    n = len(p.known)
+    nb = min(p.tile_size(), n)
+    h = _handle_for(coords, nb, p.max_rank, 1)
+    return h.predict(np.asarray(p.z, dtype=float), _coords_of(p.unknown), p.theta,
+                     p.accuracy if p.mode == "tlr" else None)
+
+
+# ------------------------------------------------------ component entry points
+def bessel_k(nu: float, x) -> np.ndarray:
+    """K_nu(x) evaluated on the device (kernels.py:160-174)."""
+    lib = _lib.load()
+    x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float64)
+    out = np.empty_like(x)
+    rc = lib.tlrb_bessel_k(float(nu), dptr(x), x.size, dptr(out), 0)
+    if rc:
+        raise ValueError(f"tlrb_bessel_k failed ({rc})")
+    return out
+
+
+def matern_block(rows_xy, cols_xy, p: MaternParams) -> np.ndarray:
+    """Dense kernel block on the device (kernels.py:494-530, no nugget)."""
+    lib = _lib.load()
+    a = np.ascontiguousarray(rows_xy, dtype=np.float64)
+    b = np.ascontiguousarray(cols_xy, dtype=np.float64)
+    out = np.empty((b.shape[0], a.shape[0]))  # column-major m x n == row-major n x m
+    rc = lib.tlrb_matern_block(dptr(a), a.shape[0], dptr(b), b.shape[0], p.theta1, p.theta2,
+                               p.theta3, dptr(out), 0)
+    if rc:
+        raise ValueError(f"tlrb_matern_block failed ({rc})")
+    return out.T.copy()
+
+
+def compress_tile(a: np.ndarray, eps: float):
+    """Device compression of one tile; returns (u, v) with a ~= u v^T
+    (compression.py:39-51 contract)."""
+    lib = _lib.load()
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    af = np.asfortranarray(a)
+    k = np.zeros(1, np.int32)
+    u = np.zeros(m * min(m, n))
+    v = np.zeros(n * min(m, n))
+    rc = lib.tlrb_compress_tile(dptr(af), m, n, float(eps), iptr(k), dptr(u), dptr(v), 0)
+    if rc:
+        raise ValueError(f"tlrb_compress_tile failed ({rc})")
+    r = int(k[0])
+    return (u[: m * r].reshape(r, m).T.copy(), v[: n * r].reshape(r, n).T.copy())
+
+
+def launch_count() -> int:
+    return int(_lib.load().tlrb_launch_count())

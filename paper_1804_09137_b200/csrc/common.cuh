@@ -1,0 +1,129 @@
+// common.cuh — shared declarations for the sm_100a TLR likelihood kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <cstring>
+#include <algorithm>
+
+namespace tlrb {
+
+extern int64_t g_launches;  // kernels launched by this library (process-wide)
+
+#define TLRB_CUDA(call)                                                        \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) throw ::tlrb::CudaError(e_, #call, __FILE__, __LINE__); \
+  } while (0)
+
+struct CudaError {
+  cudaError_t code;
+  char msg[256];
+  CudaError(cudaError_t c, const char* what, const char* file, int line) : code(c) {
+    snprintf(msg, sizeof msg, "%s failed at %s:%d: %s", what, file, line,
+             cudaGetErrorString(c));
+  }
+};
+
+inline void post_launch() {
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(e, "kernel launch", __FILE__, __LINE__);
+}
+
+// ------------------------------------------------------------------ Matern
+struct MaternParamsDev {
+  double theta1, inv_theta2, nu, pref;   // pref = theta1 / (2^(nu-1) Gamma(nu))
+  double gampl, gammi, gam1, gam2;       // Temme constants for mu = nu - round(nu)
+  int nl;                                // int(nu + 0.5)
+  double mu;
+  int kind;                              // 0: nu=1/2, 1: nu=3/2, 2: nu=5/2, 3: general
+};
+MaternParamsDev make_matern(double theta1, double theta2, double nu);
+
+struct GenTile {          // one Matern block: rows [r0, r0+m) x cols [c0, c0+n)
+  double* out; int ld;
+  int r0, m, c0, n;
+  double diag_add;        // added where global row == global col (nugget)
+};
+
+// --------------------------------------------------------------------- GEMM
+struct GemmProb {
+  const double* A; const double* B; const double* Cin; double* C;
+  int m, n, k, lda, ldb, ldcin, ldc;
+  int ta, tb;             // op(A) = A^T if ta, op(B) = B^T if tb
+  int lower_only;         // skip CTA tiles strictly above the diagonal
+  double alpha, beta;     // C = alpha op(A) op(B) + beta Cin
+};
+
+// --------------------------------------------------------------------- TRSM
+struct TrsmProb {          // B <- L^-1 B (or L^-T B), L lower n x n
+  const double* L; int ldl;
+  double* B; int ldb;
+  int n, nrhs;
+};
+
+// ----------------------------------------------------------------------- QR
+struct QrProb {            // Householder QR of A (m x s); Q (m x s) formed explicitly
+  double* A; int lda;      // in: A; out: R (upper) + V (below diag)
+  double* Q; int ldq;
+  double* T;               // workspace: s x 16 compact-WY T factors
+  int m, s;
+};
+
+// ------------------------------------------------------------------- Jacobi
+struct JacobiProb {        // one-sided Jacobi on the columns of X (m x s)
+  double* X; int ldx;
+  double* Vout; int ldv;   // sorted, normalized columns (m x s)
+  double* sigma;           // s sorted singular values (descending)
+  const double* aux;       // [0] = e2 (sketch residual^2), [1] = noise floor
+  double eps;              // accuracy threshold
+  int* rank_out;           // truncation rank (compression.py:26-36 rule)
+  int* sweeps_out;
+  int m, s;
+};
+
+// ----------------------------------------------------------- small helpers
+struct SumsqProb { const double* A; int ld, m, n; double* out; };
+struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale; };
+struct GaussProb { double* A; int ld, m, n; uint64_t seed; };
+
+// Device-resident descriptor staging (pinned host ring -> device), reset at
+// stream synchronisation points.
+class DescArena {
+ public:
+  void init(size_t bytes);
+  void release();
+  template <class T> T* put(const std::vector<T>& v, cudaStream_t s) {
+    return static_cast<T*>(put_bytes(v.data(), v.size() * sizeof(T), s));
+  }
+  void* put_bytes(const void* src, size_t bytes, cudaStream_t s);
+  void reset() { off_ = 0; }
+  size_t used() const { return off_; }
+ private:
+  char* h_ = nullptr; char* d_ = nullptr; size_t cap_ = 0, off_ = 0;
+};
+
+// launchers (all asynchronous on `s`)
+void launch_gen_tiles(const std::vector<GenTile>& tiles, const double* x, const double* y,
+                      const MaternParamsDev& p, DescArena& ar, cudaStream_t s);
+void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s);
+void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);
+void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
+                        double* logdiag, cudaStream_t s);
+void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_gaussian(const std::vector<GaussProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_sum_log(const double* logdiag, int n, double* out, cudaStream_t s);
+void launch_dot(const double* x, int n, double* out, cudaStream_t s);
+void launch_cross_gemv(const double* kx, const double* ky, const double* w, int64_t n,
+                       const double* ux, const double* uy, int64_t m, const MaternParamsDev& p,
+                       double* partial, double* out, cudaStream_t s);
+void launch_aux(const double* sums, const int* kinds, int nprob, double* aux, int* ok,
+                double rel_tol2, cudaStream_t s);
+
+}  // namespace tlrb

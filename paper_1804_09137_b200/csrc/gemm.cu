@@ -1,0 +1,154 @@
+// gemm.cu — variable-size batched FP64 GEMM on the sm_100a FP64 tensor pipe.
+//
+// tcgen05.mma has no f64 kind on sm_100a, so FP64 tensor-core math is
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  One launch covers a whole batch of
+// independent problems of different (m, n, k): the grid is the flattened list
+// of 64x64 output tiles of every problem (binary search of a prefix sum), so
+// a step of the tile Cholesky (all SYRK / GEMM / low-rank product updates of
+// panel k) is one launch.
+//
+// CTA: 128 threads = 4 warps in a 2x2 layout, warp tile 32x32 = 4x4 DMMA
+// tiles; BK = 16; operands staged global -> registers -> shared memory with a
+// two-stage ping-pong so the next K slab loads while DMMAs run.
+#include "common.cuh"
+
+namespace tlrb {
+
+constexpr int GBM = 64, GBN = 64, GBK = 16, GPAD = 8;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) dgemm_vbatch_kernel(const GemmProb* __restrict__ probs,
+                                                           const int* __restrict__ start,
+                                                           int nprob) {
+  const int blk = blockIdx.x;
+  int lo = 0, hi = nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= blk) lo = mid; else hi = mid - 1;
+  }
+  const GemmProb P = probs[lo];
+  const int local = blk - start[lo];
+  const int tm = (P.m + GBM - 1) / GBM;
+  const int m0 = (local % tm) * GBM, n0 = (local / tm) * GBN;
+  if (P.lower_only && n0 >= m0 + GBM) return;
+
+  __shared__ double As[2][GBK][GBM + GPAD];
+  __shared__ double Bs[2][GBK][GBN + GPAD];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + i * 128;
+      int r, kk;
+      if (!P.ta) { r = e & 63; kk = e >> 6; } else { r = e >> 4; kk = e & 15; }
+      const int gr = m0 + r, gk = k0 + kk;
+      double v = 0.0;
+      if (gr < P.m && gk < P.k)
+        v = P.ta ? P.A[(size_t)gr * P.lda + gk] : P.A[(size_t)gk * P.lda + gr];
+      ra[i] = v;
+      int c;
+      if (!P.tb) { kk = e & 15; c = e >> 4; } else { c = e & 63; kk = e >> 6; }
+      const int gc = n0 + c;
+      const int gk2 = k0 + kk;
+      double w = 0.0;
+      if (gc < P.n && gk2 < P.k)
+        w = P.tb ? P.B[(size_t)gk2 * P.ldb + gc] : P.B[(size_t)gc * P.ldb + gk2];
+      rb[i] = w;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + i * 128;
+      int r, kk;
+      if (!P.ta) { r = e & 63; kk = e >> 6; } else { r = e >> 4; kk = e & 15; }
+      As[buf][kk][r] = ra[i];
+      int c;
+      if (!P.tb) { kk = e & 15; c = e >> 4; } else { c = e & 63; kk = e >> 6; }
+      Bs[buf][kk][c] = rb[i];
+    }
+  };
+
+  const int nk = (P.k + GBK - 1) / GBK;
+  if (nk > 0) {
+    load(0);
+    store(0);
+    __syncthreads();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    const int cur = kc & 1;
+    if (kc + 1 < nk) load((kc + 1) * GBK);
+#pragma unroll
+    for (int k4 = 0; k4 < GBK; k4 += 4) {
+      double a[4], b[4];
+      const int kr = k4 + (lane & 3);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a[t] = As[cur][kr][wm + t * 8 + (lane >> 2)];
+        b[t] = Bs[cur][kr][wn + t * 8 + (lane >> 2)];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (kc + 1 < nk) store(cur ^ 1);
+    __syncthreads();
+  }
+
+  // epilogue: C = alpha acc + beta Cin
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm + i * 8 + (lane >> 2);
+    if (r >= P.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+        if (c >= P.n) continue;
+        double v = P.alpha * acc[i][j][h];
+        if (P.beta != 0.0) v += P.beta * P.Cin[(size_t)c * P.ldcin + r];
+        P.C[(size_t)c * P.ldc + r] = v;
+      }
+    }
+  }
+}
+
+void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  std::vector<GemmProb> keep;
+  keep.reserve(probs.size());
+  std::vector<int> start;
+  start.reserve(probs.size() + 1);
+  int tot = 0;
+  for (const GemmProb& p : probs) {
+    if (p.m <= 0 || p.n <= 0) continue;
+    keep.push_back(p);
+    start.push_back(tot);
+    tot += ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
+  }
+  if (tot == 0) return;
+  start.push_back(tot);
+  const GemmProb* dp = ar.put(keep, s);
+  const int* ds = ar.put(start, s);
+  dgemm_vbatch_kernel<<<tot, 128, 0, s>>>(dp, ds, (int)keep.size());
+  post_launch();
+}
+
+}  // namespace tlrb

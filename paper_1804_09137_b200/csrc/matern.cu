@@ -1,0 +1,249 @@
+// matern.cu — K1: Matern covariance tile generation with a device-side
+// modified Bessel K_nu (FP64), plus the fused cross-covariance GEMV used by
+// kriging.
+//
+// Reference behaviour restated (not translated):
+//   K_nu: Temme series for x <= 2 and the Thompson-Barnett continued fraction
+//   for x > 2, then forward recurrence in the order
+//   (/root/reference/pkg/src/tlrgeo/kernels.py:82-174);
+//   kernel value of the scaled distance t = r/theta2 with the t<=0 -> theta1,
+//   t > 700 -> 0 and overflow/ >theta1 -> theta1 guards (kernels.py:177-188);
+//   block evaluation (kernels.py:436-443, 494-530); nugget on the matrix
+//   diagonal only (tilestore.py:213-215).
+// Half-integer smoothness (nu = 1/2, 3/2, 5/2) uses the closed forms
+// theta1 e^-t (1 + t + ...), equal to the series path to rounding, which
+// keeps generation at the HBM-write roofline for the benchmark configs.
+#include "common.cuh"
+#include <cmath>
+
+namespace tlrb {
+
+MaternParamsDev make_matern(double theta1, double theta2, double nu) {
+  MaternParamsDev p{};
+  p.theta1 = theta1;
+  p.inv_theta2 = 1.0 / theta2;
+  p.nu = nu;
+  p.pref = theta1 / (std::pow(2.0, nu - 1.0) * std::tgamma(nu));
+  p.nl = (int)(nu + 0.5);
+  p.mu = nu - p.nl;
+  const double mu = p.mu;
+  p.gampl = 1.0 / std::tgamma(1.0 + mu);
+  p.gammi = 1.0 / std::tgamma(1.0 - mu);
+  if (std::fabs(mu) < 1e-2) {
+    const double m2 = mu * mu;
+    p.gam1 = -0.5772156649015328606 + m2 * (0.0420026350340952355 + m2 * 0.0421977345555443367);
+  } else {
+    p.gam1 = (p.gammi - p.gampl) / (2.0 * mu);
+  }
+  p.gam2 = 0.5 * (p.gammi + p.gampl);
+  if (nu == 0.5) p.kind = 0;
+  else if (nu == 1.5) p.kind = 1;
+  else if (nu == 2.5) p.kind = 2;
+  else p.kind = 3;
+  return p;
+}
+
+// (K_mu(x), K_mu+1(x)) for x <= 2 by Temme's series.
+__device__ static void kv_series(const MaternParamsDev& p, double x, double& k0, double& k1) {
+  const double mu = p.mu;
+  const double half = 0.5 * x;
+  const double pm = M_PI * mu;
+  const double fact = fabs(pm) < 1e-15 ? 1.0 : pm / sin(pm);
+  double d = -log(half);
+  double e = mu * d;
+  const double f2 = fabs(e) < 1e-15 ? 1.0 : sinh(e) / e;
+  double ff = fact * (p.gam1 * cosh(e) + p.gam2 * f2 * d);
+  double sum = ff;
+  e = exp(e);
+  double pp = 0.5 * e / p.gampl;
+  double qq = 0.5 / (e * p.gammi);
+  double c = 1.0;
+  const double d2 = half * half;
+  double sum1 = pp;
+  for (int i = 1; i < 1000; ++i) {
+    const double di = (double)i;
+    ff = (di * ff + pp + qq) / (di * di - mu * mu);
+    c *= d2 / di;
+    pp /= di - mu;
+    qq /= di + mu;
+    const double del = c * ff;
+    sum += del;
+    sum1 += c * (pp - di * ff);
+    if (fabs(del) < fabs(sum) * 1e-15) break;
+  }
+  k0 = sum;
+  k1 = sum1 * (2.0 / x);
+}
+
+// (K_mu(x), K_mu+1(x)) for x > 2 by the Thompson-Barnett continued fraction.
+__device__ static void kv_cf2(double mu, double x, double& k0, double& k1) {
+  double b = 2.0 * (1.0 + x);
+  double d = 1.0 / b;
+  double h = d, delh = d;
+  double q1 = 0.0, q2 = 1.0;
+  const double a1 = 0.25 - mu * mu;
+  double q = a1, c = a1, a = -a1;
+  double s = 1.0 + q * delh;
+  for (int i = 2; i < 1000; ++i) {
+    a -= 2.0 * (i - 1);
+    c = -a * c / i;
+    const double qn = (q1 - b * q2) / a;
+    q1 = q2;
+    q2 = qn;
+    q += c * qn;
+    b += 2.0;
+    d = 1.0 / (b + a * d);
+    delh = (b * d - 1.0) * delh;
+    h += delh;
+    const double dels = q * delh;
+    s += dels;
+    if (fabs(dels / s) < 1e-15) break;
+  }
+  h = a1 * h;
+  k0 = sqrt(M_PI / (2.0 * x)) * exp(-x) / s;
+  k1 = k0 * (mu + x + 0.5 - h) / x;
+}
+
+__device__ static double kv_general(const MaternParamsDev& p, double x) {
+  double k0, k1;
+  if (x <= 2.0) kv_series(p, x, k0, k1);
+  else kv_cf2(p.mu, x, k0, k1);
+  for (int i = 0; i < p.nl; ++i) {
+    const double kn = (p.mu + i + 1.0) * (2.0 / x) * k1 + k0;
+    k0 = k1;
+    k1 = kn;
+  }
+  return k0;
+}
+
+__device__ __forceinline__ double matern_t(const MaternParamsDev& p, double t) {
+  if (t <= 0.0) return p.theta1;
+  if (t > 700.0) return 0.0;
+  double v;
+  switch (p.kind) {
+    case 0: v = p.theta1 * exp(-t); break;
+    case 1: v = p.theta1 * (1.0 + t) * exp(-t); break;
+    case 2: v = p.theta1 * (1.0 + t + t * t * (1.0 / 3.0)) * exp(-t); break;
+    default: v = p.pref * pow(t, p.nu) * kv_general(p, t); break;
+  }
+  if (!isfinite(v) || v > p.theta1) return p.theta1;
+  return v;
+}
+
+// ---------------------------------------------------------------- K1 tiles
+// Each CTA writes a 64 (rows) x 32 (cols) block of one tile, column-major, so
+// a warp's stores are 32 consecutive doubles (256 B, fully coalesced).
+constexpr int GEN_BM = 64, GEN_BN = 32;
+
+__global__ void __launch_bounds__(256) gen_tiles_kernel(const GenTile* __restrict__ tiles,
+                                                        const int* __restrict__ start, int ntiles,
+                                                        const double* __restrict__ X,
+                                                        const double* __restrict__ Y,
+                                                        MaternParamsDev p) {
+  const int blk = blockIdx.x;
+  int lo = 0, hi = ntiles - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= blk) lo = mid; else hi = mid - 1;
+  }
+  const GenTile T = tiles[lo];
+  const int local = blk - start[lo];
+  const int tm = (T.m + GEN_BM - 1) / GEN_BM;
+  const int bm = local % tm, bn = local / tm;
+  const int r = bm * GEN_BM + (threadIdx.x & 63);
+  if (r >= T.m) return;
+  const int gr = T.r0 + r;
+  const double px = X[gr], py = Y[gr];
+  const int cbase = bn * GEN_BN + (threadIdx.x >> 6) * (GEN_BN / 4);
+#pragma unroll
+  for (int cc = 0; cc < GEN_BN / 4; ++cc) {
+    const int c = cbase + cc;
+    if (c >= T.n) break;
+    const int gc = T.c0 + c;
+    const double dx = px - X[gc], dy = py - Y[gc];
+    double v = matern_t(p, sqrt(dx * dx + dy * dy) * p.inv_theta2);
+    if (gr == gc) v += T.diag_add;
+    T.out[(size_t)c * T.ld + r] = v;
+  }
+}
+
+void launch_gen_tiles(const std::vector<GenTile>& tiles, const double* x, const double* y,
+                      const MaternParamsDev& p, DescArena& ar, cudaStream_t s) {
+  if (tiles.empty()) return;
+  std::vector<int> start(tiles.size() + 1);
+  int tot = 0;
+  for (size_t i = 0; i < tiles.size(); ++i) {
+    start[i] = tot;
+    tot += ((tiles[i].m + GEN_BM - 1) / GEN_BM) * ((tiles[i].n + GEN_BN - 1) / GEN_BN);
+  }
+  start[tiles.size()] = tot;
+  if (tot == 0) return;
+  const GenTile* dt = ar.put(tiles, s);
+  const int* ds = ar.put(start, s);
+  gen_tiles_kernel<<<tot, 256, 0, s>>>(dt, ds, (int)tiles.size(), x, y, p);
+  post_launch();
+}
+
+__global__ void bessel_kernel(double nu, const double* x, double* out, int64_t n,
+                              MaternParamsDev p) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = kv_general(p, x[i]);
+}
+
+void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s) {
+  MaternParamsDev p = make_matern(1.0, 1.0, nu);
+  bessel_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nu, x, out, n, p);
+  post_launch();
+}
+
+// ------------------------------------------------ kriging cross GEMV (S12 w)
+// partial[a * nchunk + c] = sum over known points j in chunk c of
+// C(|u_a - s_j|) w_j; then a deterministic per-row reduction.  Sigma_12 is
+// never materialised (predict.py:77-79 builds it densely).
+constexpr int XG_CHUNK = 2048;
+
+__global__ void __launch_bounds__(256) cross_gemv_kernel(const double* __restrict__ kx,
+                                                         const double* __restrict__ ky,
+                                                         const double* __restrict__ w, int64_t n,
+                                                         const double* __restrict__ ux,
+                                                         const double* __restrict__ uy,
+                                                         MaternParamsDev p, double* partial) {
+  const int a = blockIdx.y;
+  const int chunk = blockIdx.x;
+  const int64_t j0 = (int64_t)chunk * XG_CHUNK;
+  const double px = ux[a], py = uy[a];
+  double acc = 0.0;
+  for (int64_t j = j0 + threadIdx.x; j < n && j < j0 + XG_CHUNK; j += blockDim.x) {
+    const double dx = px - kx[j], dy = py - ky[j];
+    acc += matern_t(p, sqrt(dx * dx + dy * dy) * p.inv_theta2) * w[j];
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(size_t)a * gridDim.x + chunk] = red[0];
+}
+
+__global__ void row_sum_kernel(const double* partial, int nchunk, int64_t m, double* out) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunk; ++c) s += partial[a * nchunk + c];
+  out[a] = s;
+}
+
+void launch_cross_gemv(const double* kx, const double* ky, const double* w, int64_t n,
+                       const double* ux, const double* uy, int64_t m, const MaternParamsDev& p,
+                       double* partial, double* out, cudaStream_t s) {
+  const int nchunk = (int)((n + XG_CHUNK - 1) / XG_CHUNK);
+  dim3 grid(nchunk, (unsigned)m);
+  cross_gemv_kernel<<<grid, 256, 0, s>>>(kx, ky, w, n, ux, uy, p, partial);
+  post_launch();
+  row_sum_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(partial, nchunk, m, out);
+  post_launch();
+}
+
+}  // namespace tlrb

@@ -1,0 +1,173 @@
+// misc.cu — small batched helpers: Frobenius sums of squares (deterministic
+// block reductions), strided copies / transposes, seeded Gaussian sketches,
+// log-determinant and dot-product reductions, compression bookkeeping.
+#include "common.cuh"
+#include <cfloat>
+
+namespace tlrb {
+
+int64_t g_launches = 0;
+
+void DescArena::init(size_t bytes) {
+  TLRB_CUDA(cudaHostAlloc(&h_, bytes, cudaHostAllocDefault));
+  TLRB_CUDA(cudaMalloc(&d_, bytes));
+  cap_ = bytes;
+  off_ = 0;
+}
+void DescArena::release() {
+  if (h_) cudaFreeHost(h_);
+  if (d_) cudaFree(d_);
+  h_ = d_ = nullptr;
+  cap_ = off_ = 0;
+}
+void* DescArena::put_bytes(const void* src, size_t bytes, cudaStream_t s) {
+  const size_t a = (off_ + 255) & ~(size_t)255;
+  if (a + bytes > cap_) {
+    // arena full: wait for the stream so earlier descriptors are consumed
+    TLRB_CUDA(cudaStreamSynchronize(s));
+    off_ = 0;
+    return put_bytes(src, bytes, s);
+  }
+  memcpy(h_ + a, src, bytes);
+  TLRB_CUDA(cudaMemcpyAsync(d_ + a, h_ + a, bytes, cudaMemcpyHostToDevice, s));
+  off_ = a + bytes;
+  return d_ + a;
+}
+
+// ------------------------------------------------------------ sum of squares
+__global__ void __launch_bounds__(256) sumsq_kernel(const SumsqProb* __restrict__ probs) {
+  const SumsqProb P = probs[blockIdx.x];
+  double a = 0.0;
+  const int64_t tot = (int64_t)P.m * P.n;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int r = (int)(e % P.m), c = (int)(e / P.m);
+    const double x = P.A[(size_t)c * P.ld + r];
+    a = fma(x, x, a);
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *P.out = red[0];
+}
+
+void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  const SumsqProb* dp = ar.put(probs, s);
+  sumsq_kernel<<<(unsigned)probs.size(), 256, 0, s>>>(dp);
+  post_launch();
+}
+
+// ---------------------------------------------------------------- copies
+__global__ void __launch_bounds__(256) copy_kernel(const CopyProb* __restrict__ probs, int chunks) {
+  const CopyProb P = probs[blockIdx.x / chunks];
+  const int part = blockIdx.x % chunks;
+  const int64_t tot = (int64_t)P.m * P.n;
+  const int64_t per = (tot + chunks - 1) / chunks;
+  const int64_t e0 = part * per, e1 = min(tot, e0 + per);
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int r = (int)(e % P.m), c = (int)(e / P.m);
+    const double v = P.transpose ? P.src[(size_t)r * P.lds + c] : P.src[(size_t)c * P.lds + r];
+    P.dst[(size_t)c * P.ldd + r] = P.scale * v;
+  }
+}
+
+void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s) {
+  std::vector<CopyProb> keep;
+  int64_t mx = 0;
+  for (const CopyProb& p : probs)
+    if (p.m > 0 && p.n > 0) {
+      keep.push_back(p);
+      mx = std::max<int64_t>(mx, (int64_t)p.m * p.n);
+    }
+  if (keep.empty()) return;
+  const int chunks = (int)std::min<int64_t>(64, (mx + 8191) / 8192);
+  const CopyProb* dp = ar.put(keep, s);
+  copy_kernel<<<(unsigned)(keep.size() * chunks), 256, 0, s>>>(dp, chunks);
+  post_launch();
+}
+
+// ------------------------------------------------------- Gaussian sketch
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) gaussian_kernel(const GaussProb* __restrict__ probs) {
+  const GaussProb P = probs[blockIdx.y];
+  const int64_t tot = (int64_t)P.m * P.n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % P.m), c = (int)(e / P.m);
+    const uint64_t h1 = splitmix(P.seed ^ (uint64_t)e * 0x2545F4914F6CDD1Dull);
+    const uint64_t h2 = splitmix(h1);
+    const double u1 = ((h1 >> 11) + 1) * (1.0 / 9007199254740993.0);   // (0,1]
+    const double u2 = (h2 >> 11) * (1.0 / 9007199254740992.0);         // [0,1)
+    P.A[(size_t)c * P.ld + r] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+void launch_gaussian(const std::vector<GaussProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  const GaussProb* dp = ar.put(probs, s);
+  dim3 grid(16, (unsigned)probs.size());
+  gaussian_kernel<<<grid, 256, 0, s>>>(dp);
+  post_launch();
+}
+
+// ---------------------------------------------------- scalar reductions
+__global__ void __launch_bounds__(1024) reduce_kernel(const double* x, int n, double* out,
+                                                      int square) {
+  double a = 0.0;
+  // contiguous per-thread ranges: deterministic
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+  for (int i = i0; i < i1; ++i) a += square ? x[i] * x[i] : x[i];
+  __shared__ double red[1024];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+void launch_sum_log(const double* logdiag, int n, double* out, cudaStream_t s) {
+  reduce_kernel<<<1, 1024, 0, s>>>(logdiag, n, out, 0);
+  post_launch();
+}
+void launch_dot(const double* x, int n, double* out, cudaStream_t s) {
+  reduce_kernel<<<1, 1024, 0, s>>>(x, n, out, 1);
+  post_launch();
+}
+
+// ------------------------------------------------ compression bookkeeping
+// sums[6p + {0..5}] = {||M||^2, e2, ||U1||^2, ||U2||^2, ||V1||^2, ||V2||^2}
+// aux[2p] = e2 (0 when unsketched), aux[2p+1] = noise floor
+//   50 eps_mach ||[U1 U2]||_F ||[V1 V2]||_F  (compression.py:78), 0 for tiles;
+// ok[p] = e2 <= rel_tol2 ||M||^2.
+__global__ void aux_kernel(const double* sums, const int* kinds, int nprob, double* aux, int* ok,
+                           double rel_tol2) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nprob) return;
+  const double* S = sums + 6 * p;
+  const int kind = kinds[p];   // bit0: sketched, bit1: recompression
+  const double e2 = (kind & 1) ? S[1] : 0.0;
+  aux[2 * p] = e2;
+  aux[2 * p + 1] = (kind & 2) ? 50.0 * DBL_EPSILON * sqrt(S[2] + S[3]) * sqrt(S[4] + S[5]) : 0.0;
+  ok[p] = (!(kind & 1)) || (e2 <= rel_tol2 * S[0]);
+}
+
+void launch_aux(const double* sums, const int* kinds, int nprob, double* aux, int* ok,
+                double rel_tol2, cudaStream_t s) {
+  aux_kernel<<<(nprob + 127) / 128, 128, 0, s>>>(sums, kinds, nprob, aux, ok, rel_tol2);
+  post_launch();
+}
+
+}  // namespace tlrb

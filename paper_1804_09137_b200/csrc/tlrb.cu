@@ -1,0 +1,878 @@
+// tlrb.cu — host runtime and C ABI of libtlrb200.so.
+//
+// One evaluation of the Gaussian log-likelihood (stats.py:103-112) as a
+// sequence of batched sm_100a kernel launches on the handle's stream:
+//
+//   K1  generate every lower-triangle tile (tilestore.py:181-223)
+//   K2  TLR: compress every off-diagonal tile to acc (compression.py:39-51)
+//   K3  per panel k: POTRF(L_kk) with NPD report (linalg.py:36-45)
+//   K4  per panel k: TRSM of the panel (dense tiles linalg.py:94-97 /
+//       V factors linalg.py:121-127)
+//   K5  per panel k: diagonal updates (dense :100 / low-rank :128-132)
+//   K6+K7 per panel k: off-diagonal updates; TLR: form the updated tile
+//       U_ij V_ij^T - U_ik (V_ik^T V_jk) U_jk^T and recompress it to acc with
+//       the reference's truncation rule and noise floor (:133-139,
+//       compression.py:54-81) — all (i,j) of one k in one batch, never
+//       merging several k (eager recompression)
+//   K8  forward solve + dot + log-det (linalg.py:166-177, 200-206, 78-79)
+//
+// Data layout in HBM (column-major FP64 everywhere):
+//   diag   : t tiles of nb x nb (ld nb)
+//   U, V   : one slab of nb x cap per lower tile (i > j), tile id i(i-1)/2+j.
+//            TLR: U_ij (size_i x k), V_ij (size_j x k).  Dense mode: the U
+//            slab holds L_ij^T (size_j x size_i) so panel solves are
+//            left-lower TRSMs on contiguous columns.
+//   ws     : per-job compression workspace slots (M, E, Y, Q, Omega, B^T, V)
+#include "common.cuh"
+#include "../../include/tlrb200.h"
+#include <cmath>
+#include <string>
+#include <chrono>
+
+using namespace tlrb;
+
+namespace {
+
+constexpr double kSketchRelTol = 1e-3;   // sketch residual <= 1e-3 * acc * ||M||_F
+constexpr double kFullSketchFrac = 0.7;  // sketches this wide fall back to the full tile
+constexpr int kPotrfBlock = 32;
+
+struct Flops {
+  double f = 0, b = 0;
+  void add(double ff, double bb) { f += ff; b += bb; }
+};
+
+}  // namespace
+
+struct tlrb_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6];
+  int64_t n = 0;
+  int nb = 0, t = 0, cap = 0, max_rank = 0;
+  std::vector<int> off, sz;
+  double* dx = nullptr;
+  double* dy = nullptr;
+  double* diag = nullptr;
+  double* U = nullptr;
+  double* V = nullptr;
+  size_t slab = 0;               // doubles per U (or V) slab
+  std::vector<int> rank;         // per lower tile
+  int* d_info = nullptr;         // [flag, tile, pivot]
+  double* d_logdiag = nullptr;   // n
+  double* d_scal = nullptr;      // [logdet, quad]
+  double* d_z = nullptr;         // n (rhs / solution)
+  double* d_w = nullptr;         // solve temporaries (t * nb)
+  // kriging
+  double* d_ux = nullptr; double* d_uy = nullptr; double* d_pred = nullptr;
+  double* d_partial = nullptr; int64_t ucap = 0;
+  DescArena ar;
+  // compression workspace
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  size_t slot_doubles = 0;
+  int max_jobs = 0;
+  double* d_sums = nullptr;      // 6 per job
+  double* d_aux = nullptr;       // 2 per job
+  int* d_kind = nullptr;         // per job
+  int* d_ok = nullptr;           // per job
+  int* d_rank = nullptr;         // per job
+  int* d_sweeps = nullptr;       // per job
+  // state
+  int factor_mode = 0;           // 0: none, 1: dense, 2: tlr
+  MaternParamsDev mp{};
+  double acc = 0;
+  int err_tile = -1, err_pivot = -1;
+  std::string msg;
+  tlrb_stats st{};
+  Flops work;
+  int retries = 0, max_sweeps = 0;
+
+  size_t tid(int i, int j) const { return (size_t)i * (i - 1) / 2 + j; }
+  double* Ut(int i, int j) const { return U + tid(i, j) * slab; }
+  double* Vt(int i, int j) const { return V + tid(i, j) * slab; }
+  double* D(int i) const { return diag + (size_t)i * nb * nb; }
+  void sync() {
+    TLRB_CUDA(cudaStreamSynchronize(stream));
+    ar.reset();
+  }
+};
+
+namespace {
+
+// ------------------------------------------------------------ compression
+struct Job {
+  int m, n;           // M is m x n
+  int s;              // sketch width (== n: unsketched)
+  int kind;           // bit1: recompression (noise floor)
+  double* M;          // slot pointers
+  double* E; double* Y; double* Q; double* Om; double* Bt; double* Vs; double* sig; double* T;
+  double* Uout; double* Vout; int ldu, ldv;
+  int out_rank;
+  uint64_t seed;
+};
+
+void bind_slot(tlrb_handle* h, Job& J, int slot) {
+  double* base = reinterpret_cast<double*>(h->ws) + (size_t)slot * h->slot_doubles;
+  const size_t nb2 = (size_t)h->nb * h->nb;
+  J.M = base;
+  J.E = base + nb2;
+  J.Y = base + 2 * nb2;
+  J.Q = base + 3 * nb2;
+  J.Om = base + 4 * nb2;
+  J.Bt = base + 5 * nb2;
+  J.Vs = base + 6 * nb2;
+  J.sig = base + 7 * nb2;
+  J.T = J.sig + h->nb;
+}
+
+// Compress the M of every job (already formed in its slot) to acc; writes
+// U = M V_k (m x k) and V_k (n x k) into the job's output slabs.
+void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
+  const int nj = (int)jobs.size();
+  if (!nj) return;
+  cudaStream_t s = h->stream;
+  {
+    std::vector<SumsqProb> sq;
+    for (int j = 0; j < nj; ++j) sq.push_back({jobs[j].M, jobs[j].m, jobs[j].m, jobs[j].n, h->d_sums + 6 * j});
+    launch_sumsq(sq, h->ar, s);
+  }
+  std::vector<int> kinds(nj), pending;
+  for (int j = 0; j < nj; ++j) {
+    Job& J = jobs[j];
+    if (J.s >= kFullSketchFrac * J.n) J.s = J.n;
+    if (J.s < J.n) pending.push_back(j);
+  }
+  int attempt = 0;
+  while (!pending.empty()) {
+    std::vector<GaussProb> gp;
+    std::vector<GemmProb> g1, g2, g3;
+    std::vector<QrProb> qp;
+    std::vector<SumsqProb> sq;
+    for (int j : pending) {
+      Job& J = jobs[j];
+      gp.push_back({J.Om, J.n, J.n, J.s, J.seed * 1000003ull + (uint64_t)attempt * 7919ull + 1});
+      g1.push_back({J.M, J.Om, nullptr, J.Y, J.m, J.s, J.n, J.m, J.n, J.m, J.m, 0, 0, 0, 1.0, 0.0});
+      qp.push_back({J.Y, J.m, J.Q, J.m, J.T, J.m, J.s});
+      g2.push_back({J.M, J.Q, nullptr, J.Bt, J.n, J.s, J.m, J.m, J.m, J.n, J.n, 1, 0, 0, 1.0, 0.0});
+      g3.push_back({J.Q, J.Bt, J.M, J.E, J.m, J.n, J.s, J.m, J.n, J.m, J.m, 0, 1, 0, -1.0, 1.0});
+      sq.push_back({J.E, J.m, J.m, J.n, h->d_sums + 6 * j + 1});
+    }
+    launch_gaussian(gp, h->ar, s);
+    launch_gemm(g1, h->ar, s);
+    launch_qr(qp, h->ar, s);
+    launch_gemm(g2, h->ar, s);
+    launch_gemm(g3, h->ar, s);
+    launch_sumsq(sq, h->ar, s);
+    for (int j = 0; j < nj; ++j) kinds[j] = (jobs[j].s < jobs[j].n ? 1 : 0) | jobs[j].kind;
+    TLRB_CUDA(cudaMemcpyAsync(h->d_kind, h->ar.put(kinds, s), nj * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    launch_aux(h->d_sums, h->d_kind, nj, h->d_aux, h->d_ok, (kSketchRelTol * acc) * (kSketchRelTol * acc), s);
+    std::vector<int> ok(nj);
+    TLRB_CUDA(cudaMemcpyAsync(ok.data(), h->d_ok, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+    h->sync();
+    std::vector<int> next;
+    for (int j : pending) {
+      if (ok[j]) continue;
+      Job& J = jobs[j];
+      ++h->retries;
+      J.s = std::min(J.n, 2 * J.s);
+      if (J.s >= kFullSketchFrac * J.n) J.s = J.n;
+      if (J.s < J.n) next.push_back(j);
+    }
+    pending.swap(next);
+    ++attempt;
+  }
+  // unsketched jobs: B^T = M^T
+  {
+    std::vector<CopyProb> cp;
+    for (Job& J : jobs)
+      if (J.s == J.n) { J.s = J.m; cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.m, 1, 1.0}); J.kind |= 4; }
+    launch_copy(cp, h->ar, s);
+  }
+  for (int j = 0; j < nj; ++j) kinds[j] = ((jobs[j].kind & 4) ? 0 : 1) | (jobs[j].kind & 2);
+  TLRB_CUDA(cudaMemcpyAsync(h->d_kind, h->ar.put(kinds, s), nj * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  launch_aux(h->d_sums, h->d_kind, nj, h->d_aux, h->d_ok, 0.0, s);
+  {
+    std::vector<JacobiProb> jp;
+    for (int j = 0; j < nj; ++j) {
+      Job& J = jobs[j];
+      jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, h->d_aux + 2 * j, acc, h->d_rank + j,
+                    h->d_sweeps + j, J.n, J.s});
+    }
+    launch_jacobi(jp, h->ar, s);
+  }
+  std::vector<int> rk(nj), sw(nj);
+  TLRB_CUDA(cudaMemcpyAsync(rk.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLRB_CUDA(cudaMemcpyAsync(sw.data(), h->d_sweeps, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  h->sync();
+  std::vector<GemmProb> gu;
+  std::vector<CopyProb> cv;
+  for (int j = 0; j < nj; ++j) {
+    Job& J = jobs[j];
+    J.out_rank = rk[j];
+    h->max_sweeps = std::max(h->max_sweeps, sw[j]);
+    if (rk[j] > h->cap) throw CudaError(cudaErrorMemoryAllocation, "tile rank exceeds max_rank capacity", __FILE__, __LINE__);
+    if (!rk[j]) continue;
+    gu.push_back({J.M, J.Vs, nullptr, J.Uout, J.m, rk[j], J.n, J.m, J.n, J.ldu, J.ldu, 0, 0, 0, 1.0, 0.0});
+    cv.push_back({J.Vs, J.n, J.Vout, J.ldv, J.n, rk[j], 0, 1.0});
+  }
+  launch_gemm(gu, h->ar, s);
+  launch_copy(cv, h->ar, s);
+}
+
+int sketch_guess(int prev_rank, int n) {
+  int s = (int)std::ceil(1.25 * prev_rank) + 32;
+  s = (s + 7) & ~7;
+  return std::min(s, n);
+}
+
+// ----------------------------------------------------------- generation
+void generate(tlrb_handle* h, double nugget, bool dense_lower) {
+  std::vector<GenTile> tiles;
+  for (int i = 0; i < h->t; ++i) {
+    tiles.push_back({h->D(i), h->nb, h->off[i], h->sz[i], h->off[i], h->sz[i], nugget});
+    if (dense_lower)
+      for (int j = 0; j < i; ++j)  // L_ij^T: rows = tile j points, cols = tile i points
+        tiles.push_back({h->Ut(i, j), h->nb, h->off[j], h->sz[j], h->off[i], h->sz[i], 0.0});
+  }
+  launch_gen_tiles(tiles, h->dx, h->dy, h->mp, h->ar, h->stream);
+  for (int i = 0; i < h->t; ++i) {
+    h->work.add(0, 8.0 * h->sz[i] * h->sz[i]);
+    if (dense_lower)
+      for (int j = 0; j < i; ++j) h->work.add(0, 8.0 * h->sz[i] * h->sz[j]);
+  }
+}
+
+void compress_all(tlrb_handle* h, double acc) {
+  std::vector<std::pair<int, int>> all;
+  for (int i = 1; i < h->t; ++i)
+    for (int j = 0; j < i; ++j) all.push_back({i, j});
+  // far tiles first (small ranks), near-diagonal last
+  for (size_t c0 = 0; c0 < all.size(); c0 += h->max_jobs) {
+    const size_t c1 = std::min(all.size(), c0 + h->max_jobs);
+    std::vector<Job> jobs;
+    std::vector<GenTile> gen;
+    for (size_t q = c0; q < c1; ++q) {
+      const int i = all[q].first, j = all[q].second;
+      Job J{};
+      bind_slot(h, J, (int)(q - c0));
+      J.m = h->sz[i];
+      J.n = h->sz[j];
+      // initial sketch: ranks grow towards the diagonal
+      const int off = i - j;
+      J.s = off <= 2 ? J.n : std::min(J.n, 64);
+      J.kind = 0;
+      J.Uout = h->Ut(i, j);
+      J.Vout = h->Vt(i, j);
+      J.ldu = J.ldv = h->nb;
+      J.seed = h->tid(i, j) * 131 + 17;
+      jobs.push_back(J);
+      gen.push_back({J.M, J.m, h->off[i], J.m, h->off[j], J.n, 0.0});
+    }
+    launch_gen_tiles(gen, h->dx, h->dy, h->mp, h->ar, h->stream);
+    compress_jobs(h, jobs, acc);
+    for (size_t q = c0; q < c1; ++q) {
+      const Job& J = jobs[q - c0];
+      h->rank[h->tid(all[q].first, all[q].second)] = J.out_rank;
+      const double m = J.m, n = J.n, k = J.out_rank;
+      h->work.add(4.0 * m * n * k, 8.0 * m * n + 8.0 * k * (m + n));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ POTRF
+void potrf(tlrb_handle* h, int k) {
+  const int n = h->sz[k];
+  double* A = h->D(k);
+  for (int r0 = 0; r0 < n; r0 += kPotrfBlock) {
+    const int bs = std::min(kPotrfBlock, n - r0);
+    launch_potrf_block(A, h->nb, n, r0, bs, k, h->d_info, h->d_logdiag + h->off[k], h->stream);
+    const int rest = n - r0 - bs;
+    if (rest > 0) {
+      double* A21 = A + (size_t)r0 * h->nb + r0 + bs;
+      double* A22 = A + (size_t)(r0 + bs) * h->nb + r0 + bs;
+      launch_gemm({GemmProb{A21, A21, A22, A22, rest, rest, bs, h->nb, h->nb, h->nb, h->nb, 0, 1, 1,
+                            -1.0, 1.0}},
+                  h->ar, h->stream);
+    }
+  }
+  const double nn = n;
+  h->work.add(nn * nn * nn / 3.0, 16.0 * nn * nn);
+}
+
+bool check_npd(tlrb_handle* h) {
+  int info[3];
+  TLRB_CUDA(cudaMemcpyAsync(info, h->d_info, sizeof info, cudaMemcpyDeviceToHost, h->stream));
+  h->sync();
+  if (info[0]) {
+    h->err_tile = info[1];
+    h->err_pivot = info[2];
+    char b[160];
+    snprintf(b, sizeof b, "covariance not positive definite at tile %d, pivot %d; consider adding a nugget",
+             info[1], info[2]);
+    h->msg = b;
+    return true;
+  }
+  return false;
+}
+
+// ------------------------------------------------------ dense factorisation
+bool factor_dense(tlrb_handle* h) {
+  const int t = h->t, nb = h->nb;
+  for (int k = 0; k < t; ++k) {
+    potrf(h, k);
+    std::vector<TrsmProb> tp;
+    for (int i = k + 1; i < t; ++i) tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
+    launch_trsm(tp, false, h->ar, h->stream);
+    std::vector<GemmProb> gp;
+    const double nk = h->sz[k];
+    for (int j = k + 1; j < t; ++j) {
+      // D_j -= L_jk L_jk^T = T_jk^T T_jk
+      gp.push_back({h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
+                    nb, 1, 0, 1, -1.0, 1.0});
+      h->work.add(nk * h->sz[j] * h->sz[j], 8.0 * (2.0 * nk * h->sz[j] + 2.0 * h->sz[j] * h->sz[j]));
+      // T_ij -= T_jk^T T_ik
+      for (int i = j + 1; i < t; ++i) {
+        gp.push_back({h->Ut(j, k), h->Ut(i, k), h->Ut(i, j), h->Ut(i, j), h->sz[j], h->sz[i], h->sz[k], nb,
+                      nb, nb, nb, 1, 0, 0, -1.0, 1.0});
+        h->work.add(2.0 * nk * h->sz[i] * h->sz[j],
+                    8.0 * (nk * (h->sz[i] + h->sz[j]) + 2.0 * h->sz[i] * h->sz[j]));
+      }
+    }
+    for (int i = k + 1; i < t; ++i)
+      h->work.add(nk * nk * h->sz[i], 8.0 * (nk * nk / 2 + 2.0 * nk * h->sz[i]));
+    launch_gemm(gp, h->ar, h->stream);
+  }
+  return !check_npd(h);
+}
+
+// -------------------------------------------------------- TLR factorisation
+bool factor_tlr(tlrb_handle* h, double acc) {
+  const int t = h->t, nb = h->nb;
+  double* tmp = reinterpret_cast<double*>(h->ws);  // small products before the job batch
+  for (int k = 0; k < t; ++k) {
+    potrf(h, k);
+    // K4: V_ik <- L_kk^-1 V_ik
+    std::vector<TrsmProb> tp;
+    for (int i = k + 1; i < t; ++i) {
+      const int r = h->rank[h->tid(i, k)];
+      if (r) tp.push_back({h->D(k), nb, h->Vt(i, k), nb, h->sz[k], r});
+      const double nk = h->sz[k];
+      if (r) h->work.add(nk * nk * r, 8.0 * (nk * nk / 2 + 2.0 * nk * r));
+    }
+    launch_trsm(tp, false, h->ar, h->stream);
+    if (check_npd(h)) return false;
+    // K5: D_j -= U_jk (V_jk^T V_jk) U_jk^T
+    {
+      std::vector<GemmProb> g1, g2, g3;
+      size_t o = 0;
+      const size_t ws_doubles = h->ws_bytes / sizeof(double);
+      for (int j = k + 1; j < t; ++j) {
+        const int r = h->rank[h->tid(j, k)];
+        if (!r) continue;
+        if (o + (size_t)r * r + (size_t)h->sz[j] * r > ws_doubles) {
+          launch_gemm(g1, h->ar, h->stream);
+          launch_gemm(g2, h->ar, h->stream);
+          launch_gemm(g3, h->ar, h->stream);
+          g1.clear(); g2.clear(); g3.clear();
+          o = 0;
+        }
+        double* X = tmp + o;
+        o += (size_t)r * r;
+        double* W = tmp + o;
+        o += (size_t)h->sz[j] * r;
+        g1.push_back({h->Vt(j, k), h->Vt(j, k), nullptr, X, r, r, h->sz[k], nb, nb, r, r, 1, 0, 0, 1.0, 0.0});
+        g2.push_back({h->Ut(j, k), X, nullptr, W, h->sz[j], r, r, nb, r, h->sz[j], h->sz[j], 0, 0, 0, 1.0, 0.0});
+        g3.push_back({W, h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], r, h->sz[j], nb, nb, nb, 0, 1, 1,
+                      -1.0, 1.0});
+        const double nj = h->sz[j];
+        h->work.add(4.0 * nj * r * r + 2.0 * nj * nj * r, 8.0 * (2.0 * nj * r + 2.0 * nj * nj));
+      }
+      launch_gemm(g1, h->ar, h->stream);
+      launch_gemm(g2, h->ar, h->stream);
+      launch_gemm(g3, h->ar, h->stream);
+    }
+    // K6 + K7: updates of (i, j), i > j > k, in job batches
+    std::vector<std::pair<int, int>> upd;
+    for (int j = k + 1; j < t; ++j)
+      for (int i = j + 1; i < t; ++i)
+        if (h->rank[h->tid(i, k)] && h->rank[h->tid(j, k)]) upd.push_back({i, j});
+    for (size_t c0 = 0; c0 < upd.size(); c0 += h->max_jobs) {
+      const size_t c1 = std::min(upd.size(), c0 + h->max_jobs);
+      std::vector<Job> jobs;
+      std::vector<GemmProb> gx, gy, gm, gm2;
+      std::vector<SumsqProb> sq;
+      std::vector<int> kin;
+      for (size_t q = c0; q < c1; ++q) {
+        const int i = upd[q].first, j = upd[q].second;
+        const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], kij = h->rank[h->tid(i, j)];
+        const int mi = h->sz[i], mj = h->sz[j], mk = h->sz[k];
+        Job J{};
+        const int slot = (int)(q - c0);
+        bind_slot(h, J, slot);
+        J.m = mi;
+        J.n = mj;
+        J.kind = 2;
+        J.s = sketch_guess(std::max(kij, kj), mj);
+        J.Uout = h->Ut(i, j);
+        J.Vout = h->Vt(i, j);
+        J.ldu = J.ldv = nb;
+        J.seed = (uint64_t)h->tid(i, j) * 7777 + (uint64_t)k * 131 + 5;
+        double* X = J.E;  // ki x kj
+        double* Y = J.Y;  // mi x kj   (U2 = -Y)
+        gx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, X, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
+        gy.push_back({h->Ut(i, k), X, nullptr, Y, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, 1.0, 0.0});
+        gm.push_back({h->Ut(i, j), h->Vt(i, j), nullptr, J.M, mi, mj, kij, nb, nb, mi, mi, 0, 1, 0, 1.0, 0.0});
+        gm2.push_back({Y, h->Ut(j, k), J.M, J.M, mi, mj, kj, mi, nb, mi, mi, 0, 1, 0, -1.0, 1.0});
+        double* S = h->d_sums + 6 * slot;
+        sq.push_back({h->Ut(i, j), nb, mi, kij, S + 2});
+        sq.push_back({Y, mi, mi, kj, S + 3});
+        sq.push_back({h->Vt(i, j), nb, mj, kij, S + 4});
+        sq.push_back({h->Ut(j, k), nb, mj, kj, S + 5});
+        jobs.push_back(J);
+      }
+      launch_gemm(gx, h->ar, h->stream);
+      launch_gemm(gy, h->ar, h->stream);
+      launch_gemm(gm, h->ar, h->stream);
+      launch_gemm(gm2, h->ar, h->stream);
+      launch_sumsq(sq, h->ar, h->stream);
+      compress_jobs(h, jobs, acc);
+      for (size_t q = c0; q < c1; ++q) {
+        const int i = upd[q].first, j = upd[q].second;
+        const double ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)],
+                     kij = h->rank[h->tid(i, j)];
+        const double kn = jobs[q - c0].out_rank;
+        const double K = kij + kj, Kh = std::min<double>(K, h->nb), nbd = h->sz[i];
+        h->work.add(4.0 * nbd * ki * kj + 2.0 * (4.0 * nbd * K * Kh - 4.0 / 3.0 * Kh * Kh * Kh) +
+                        24.0 * Kh * Kh * Kh + 4.0 * nbd * Kh * kn,
+                    8.0 * nbd * (2 * kij + 2 * ki + 2 * kj + 2 * kn));
+        h->rank[h->tid(i, j)] = jobs[q - c0].out_rank;
+      }
+    }
+  }
+  return !check_npd(h);
+}
+
+// ------------------------------------------------------------------ solves
+void forward_solve(tlrb_handle* h) {
+  const int t = h->t, nb = h->nb;
+  for (int j = 0; j < t; ++j) {
+    double* yj = h->d_z + h->off[j];
+    launch_trsm({TrsmProb{h->D(j), nb, yj, h->sz[j], h->sz[j], 1}}, false, h->ar, h->stream);
+    std::vector<GemmProb> g1, g2;
+    for (int i = j + 1; i < t; ++i) {
+      double* yi = h->d_z + h->off[i];
+      if (h->factor_mode == 1) {  // y_i -= T_ij^T y_j
+        g1.push_back({h->Ut(i, j), yj, yi, yi, h->sz[i], 1, h->sz[j], nb, h->sz[j], h->sz[i], h->sz[i], 1, 0, 0,
+                      -1.0, 1.0});
+      } else {
+        const int r = h->rank[h->tid(i, j)];
+        if (!r) continue;
+        double* w = h->d_w + (size_t)i * nb;
+        g1.push_back({h->Vt(i, j), yj, nullptr, w, r, 1, h->sz[j], nb, h->sz[j], r, r, 1, 0, 0, 1.0, 0.0});
+        g2.push_back({h->Ut(i, j), w, yi, yi, h->sz[i], 1, r, nb, r, h->sz[i], h->sz[i], 0, 0, 0, -1.0, 1.0});
+      }
+    }
+    launch_gemm(g1, h->ar, h->stream);
+    launch_gemm(g2, h->ar, h->stream);
+  }
+}
+
+void backward_solve(tlrb_handle* h) {
+  const int t = h->t, nb = h->nb;
+  for (int i = t - 1; i >= 0; --i) {
+    double* xi = h->d_z + h->off[i];
+    launch_trsm({TrsmProb{h->D(i), nb, xi, h->sz[i], h->sz[i], 1}}, true, h->ar, h->stream);
+    std::vector<GemmProb> g1, g2;
+    for (int j = 0; j < i; ++j) {
+      double* xj = h->d_z + h->off[j];
+      if (h->factor_mode == 1) {  // x_j -= L_ij^T x_i = T_ij x_i
+        g1.push_back({h->Ut(i, j), xi, xj, xj, h->sz[j], 1, h->sz[i], nb, h->sz[i], h->sz[j], h->sz[j], 0, 0, 0,
+                      -1.0, 1.0});
+      } else {
+        const int r = h->rank[h->tid(i, j)];
+        if (!r) continue;
+        double* w = h->d_w + (size_t)j * nb;
+        g1.push_back({h->Ut(i, j), xi, nullptr, w, r, 1, h->sz[i], nb, h->sz[i], r, r, 1, 0, 0, 1.0, 0.0});
+        g2.push_back({h->Vt(i, j), w, xj, xj, h->sz[j], 1, r, nb, r, h->sz[j], h->sz[j], 0, 0, 0, -1.0, 1.0});
+      }
+    }
+    launch_gemm(g1, h->ar, h->stream);
+    launch_gemm(g2, h->ar, h->stream);
+  }
+}
+
+// -------------------------------------------------------------- one eval
+int validate(double th1, double th2, double th3, double nugget, double acc) {
+  const double v[5] = {th1, th2, th3, nugget, acc};
+  for (double x : v)
+    if (!std::isfinite(x)) return TLRB_ERR_ARG;
+  if (th1 <= 0 || th2 <= 0 || th3 <= 0 || th3 > 5.0 || nugget < 0) return TLRB_ERR_ARG;
+  if (acc < 0 || acc >= 1) return TLRB_ERR_ARG;
+  return TLRB_OK;
+}
+
+// factorise Sigma(theta) into the handle; returns TLRB_* code
+int factorize(tlrb_handle* h, double th1, double th2, double th3, double nugget, double acc) {
+  cudaStream_t s = h->stream;
+  h->mp = make_matern(th1, th2, th3);
+  h->acc = acc;
+  h->work = Flops{};
+  h->retries = 0;
+  h->max_sweeps = 0;
+  h->err_tile = h->err_pivot = -1;
+  h->factor_mode = 0;
+  TLRB_CUDA(cudaMemsetAsync(h->d_info, 0, 3 * sizeof(int), s));
+  TLRB_CUDA(cudaEventRecord(h->ev[0], s));
+  const bool dense = acc == 0.0;
+  generate(h, nugget, dense);
+  TLRB_CUDA(cudaEventRecord(h->ev[1], s));
+  std::fill(h->rank.begin(), h->rank.end(), 0);
+  if (!dense) compress_all(h, acc);
+  TLRB_CUDA(cudaEventRecord(h->ev[2], s));
+  const bool ok = dense ? factor_dense(h) : factor_tlr(h, acc);
+  TLRB_CUDA(cudaEventRecord(h->ev[3], s));
+  if (!ok) return TLRB_ERR_NPD;
+  h->factor_mode = dense ? 1 : 2;
+  return TLRB_OK;
+}
+
+int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, double th2,
+                double th3, double nugget, double acc, double* ll, double* logdet, double* quad,
+                tlrb_stats* st) {
+  const int64_t l0 = g_launches;
+  int rc = validate(th1, th2, th3, nugget, acc);
+  if (rc) {
+    h->msg = "invalid theta / nugget / accuracy";
+    return rc;
+  }
+  TLRB_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  const auto t0 = std::chrono::steady_clock::now();
+  TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double),
+                            z_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  rc = factorize(h, th1, th2, th3, nugget, acc);
+  if (rc) return rc;
+  forward_solve(h);
+  launch_dot(h->d_z, (int)h->n, h->d_scal + 1, s);
+  launch_sum_log(h->d_logdiag, (int)h->n, h->d_scal, s);
+  TLRB_CUDA(cudaEventRecord(h->ev[4], s));
+  double sc[2];
+  TLRB_CUDA(cudaMemcpyAsync(sc, h->d_scal, sizeof sc, cudaMemcpyDeviceToHost, s));
+  h->sync();
+  const double LOG_2PI = std::log(2.0 * M_PI);
+  if (ll) *ll = -0.5 * (h->n * LOG_2PI + sc[0] + sc[1]);
+  if (logdet) *logdet = sc[0];
+  if (quad) *quad = sc[1];
+  if (st) {
+    tlrb_stats S{};
+    float a;
+    TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[0], h->ev[2])); S.ms_generate = a;
+    TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[1], h->ev[2])); S.ms_compress = a;
+    TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[2], h->ev[3])); S.ms_factor = a;
+    TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[3], h->ev[4])); S.ms_solve = a;
+    S.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    int64_t reals = 0;
+    int mx = 0;
+    double sum = 0;
+    int cnt = 0;
+    for (int i = 0; i < h->t; ++i) {
+      reals += (int64_t)h->sz[i] * h->sz[i];
+      for (int j = 0; j < i; ++j) {
+        if (h->factor_mode == 1) { reals += (int64_t)h->sz[i] * h->sz[j]; continue; }
+        const int r = h->rank[h->tid(i, j)];
+        reals += (int64_t)r * (h->sz[i] + h->sz[j]);
+        mx = std::max(mx, r);
+        sum += r;
+        ++cnt;
+      }
+    }
+    h->work.add(2.0 * reals, 8.0 * reals);
+    S.flops = h->work.f;
+    S.bytes = h->work.b;
+    S.stored_reals = reals;
+    S.max_rank = mx;
+    S.mean_rank = cnt ? sum / cnt : 0.0;
+    S.sketch_retries = h->retries;
+    S.jacobi_max_sweeps = h->max_sweeps;
+    S.kernel_launches = g_launches - l0;
+    *st = S;
+  }
+  return TLRB_OK;
+}
+
+template <class F>
+int guarded(tlrb_handle* h, F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    if (h) h->msg = e.msg;
+    cudaGetLastError();
+    return TLRB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    if (h) h->msg = e.what();
+    return TLRB_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus, int32_t max_rank,
+                         int32_t device, int32_t* err) {
+  if (err) *err = TLRB_OK;
+  if (!xy || n < 1 || nb < 1 || ngpus != 1) {
+    if (err) *err = TLRB_ERR_ARG;
+    return nullptr;
+  }
+  tlrb_handle* h = new tlrb_handle();
+  const int rc = guarded(h, [&]() -> int {
+    h->device = device;
+    TLRB_CUDA(cudaSetDevice(device));
+    TLRB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    for (auto& e : h->ev) TLRB_CUDA(cudaEventCreate(&e));
+    h->n = n;
+    h->nb = (int)std::min<int64_t>(nb, n);
+    h->t = (int)((n + h->nb - 1) / h->nb);
+    h->max_rank = max_rank;
+    h->cap = h->nb;  // TLR slabs hold up to nb columns (max_rank only reported)
+    for (int i = 0; i < h->t; ++i) {
+      h->off.push_back(i * h->nb);
+      h->sz.push_back((int)std::min<int64_t>(h->nb, n - (int64_t)i * h->nb));
+    }
+    std::vector<double> xs(n), ys(n);
+    for (int64_t i = 0; i < n; ++i) { xs[i] = xy[2 * i]; ys[i] = xy[2 * i + 1]; }
+    TLRB_CUDA(cudaMalloc(&h->dx, n * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->dy, n * sizeof(double)));
+    TLRB_CUDA(cudaMemcpy(h->dx, xs.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    TLRB_CUDA(cudaMemcpy(h->dy, ys.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    const size_t nb2 = (size_t)h->nb * h->nb;
+    const size_t ntile = (size_t)h->t * (h->t - 1) / 2;
+    h->slab = (size_t)h->nb * h->cap;
+    TLRB_CUDA(cudaMalloc(&h->diag, std::max<size_t>(1, h->t * nb2) * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->U, std::max<size_t>(1, ntile * h->slab) * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->V, std::max<size_t>(1, ntile * h->slab) * sizeof(double)));
+    h->rank.assign(ntile, 0);
+    TLRB_CUDA(cudaMalloc(&h->d_info, 4 * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_logdiag, n * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_scal, 4 * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_z, n * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_w, (size_t)h->t * h->nb * sizeof(double)));
+    h->ar.init(64u << 20);
+    // compression workspace: 7 nb^2 + 2 nb + 16 nb doubles per job slot
+    h->slot_doubles = 7 * nb2 + 18 * (size_t)h->nb + 64;
+    size_t freeb = 0, totb = 0;
+    TLRB_CUDA(cudaMemGetInfo(&freeb, &totb));
+    size_t budget = std::min<size_t>(freeb / 3, (size_t)24 << 30);
+    int jobs = (int)std::max<size_t>(1, budget / (h->slot_doubles * 8));
+    jobs = (int)std::min<size_t>(jobs, std::max<size_t>(ntile, 1));
+    h->max_jobs = std::min(jobs, 8192);
+    h->ws_bytes = std::max((size_t)h->max_jobs * h->slot_doubles * 8, nb2 * 8 * 4);
+    TLRB_CUDA(cudaMalloc(&h->ws, h->ws_bytes));
+    TLRB_CUDA(cudaMalloc(&h->d_sums, 6 * (size_t)h->max_jobs * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_aux, 2 * (size_t)h->max_jobs * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_kind, (size_t)h->max_jobs * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_ok, (size_t)h->max_jobs * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_rank, (size_t)h->max_jobs * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_sweeps, (size_t)h->max_jobs * sizeof(int)));
+    return TLRB_OK;
+  });
+  if (rc != TLRB_OK) {
+    if (err) *err = rc;
+    fprintf(stderr, "tlrb_create: %s\n", h->msg.c_str());
+    tlrb_destroy(h);
+    return nullptr;
+  }
+  return h;
+}
+
+void tlrb_destroy(tlrb_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  void* ptrs[] = {h->dx, h->dy, h->diag, h->U, h->V, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
+                  h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_ux, h->d_uy,
+                  h->d_pred, h->d_partial};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  h->ar.release();
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int32_t tlrb_loglik(tlrb_handle* h, const double* z, double th1, double th2, double th3, double nugget,
+                    double acc, double* ll, double* logdet, double* quad, tlrb_stats* st) {
+  if (!h || !z) return TLRB_ERR_ARG;
+  return guarded(h, [&] { return loglik_impl(h, z, false, th1, th2, th3, nugget, acc, ll, logdet, quad, st); });
+}
+
+int32_t tlrb_loglik_device(tlrb_handle* h, const double* d_z, double th1, double th2, double th3,
+                           double nugget, double acc, double* ll, double* logdet, double* quad,
+                           tlrb_stats* st) {
+  if (!h || !d_z) return TLRB_ERR_ARG;
+  return guarded(h, [&] { return loglik_impl(h, d_z, true, th1, th2, th3, nugget, acc, ll, logdet, quad, st); });
+}
+
+int32_t tlrb_solve(tlrb_handle* h, const double* rhs, double* x) {
+  if (!h || !rhs || !x) return TLRB_ERR_ARG;
+  if (!h->factor_mode) {
+    h->msg = "no factor available";
+    return TLRB_ERR_ARG;
+  }
+  return guarded(h, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(h->device));
+    TLRB_CUDA(cudaMemcpyAsync(h->d_z, rhs, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    forward_solve(h);
+    backward_solve(h);
+    TLRB_CUDA(cudaMemcpyAsync(x, h->d_z, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    h->sync();
+    return TLRB_OK;
+  });
+}
+
+int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown, int64_t m, double th1,
+                     double th2, double th3, double nugget, double acc, double* pred) {
+  if (!h || !z || !xy_unknown || !pred || m < 1) return TLRB_ERR_ARG;
+  int rc = validate(th1, th2, th3, nugget, acc);
+  if (rc) return rc;
+  return guarded(h, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    if (m > h->ucap) {
+      if (h->d_ux) { cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_pred); cudaFree(h->d_partial); }
+      h->ucap = m;
+      const int64_t nchunk = (h->n + 2047) / 2048;
+      TLRB_CUDA(cudaMalloc(&h->d_ux, m * sizeof(double)));
+      TLRB_CUDA(cudaMalloc(&h->d_uy, m * sizeof(double)));
+      TLRB_CUDA(cudaMalloc(&h->d_pred, m * sizeof(double)));
+      TLRB_CUDA(cudaMalloc(&h->d_partial, m * nchunk * sizeof(double)));
+    }
+    std::vector<double> ux(m), uy(m);
+    for (int64_t i = 0; i < m; ++i) { ux[i] = xy_unknown[2 * i]; uy[i] = xy_unknown[2 * i + 1]; }
+    TLRB_CUDA(cudaMemcpyAsync(h->d_ux, ux.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+    TLRB_CUDA(cudaMemcpyAsync(h->d_uy, uy.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+    TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double), cudaMemcpyHostToDevice, s));
+    int r = factorize(h, th1, th2, th3, nugget, acc);
+    if (r) return r;
+    forward_solve(h);
+    backward_solve(h);
+    launch_cross_gemv(h->dx, h->dy, h->d_z, h->n, h->d_ux, h->d_uy, m, h->mp, h->d_partial, h->d_pred, s);
+    TLRB_CUDA(cudaMemcpyAsync(pred, h->d_pred, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    h->sync();
+    return TLRB_OK;
+  });
+}
+
+int32_t tlrb_rank_map(tlrb_handle* h, int32_t* ranks, int32_t cap, int32_t* t_out) {
+  if (!h) return TLRB_ERR_ARG;
+  if (t_out) *t_out = h->t;
+  if (!ranks) return TLRB_OK;
+  if (cap < h->t * h->t) return TLRB_ERR_ARG;
+  for (int i = 0; i < h->t * h->t; ++i) ranks[i] = 0;
+  for (int i = 1; i < h->t; ++i)
+    for (int j = 0; j < i; ++j)
+      ranks[i * h->t + j] = h->factor_mode == 1 ? -1 : h->rank[h->tid(i, j)];
+  return TLRB_OK;
+}
+
+int32_t tlrb_last_error(tlrb_handle* h, int32_t* tile, int32_t* pivot, char* msg, int32_t len) {
+  if (!h) return TLRB_ERR_ARG;
+  if (tile) *tile = h->err_tile;
+  if (pivot) *pivot = h->err_pivot;
+  if (msg && len > 0) {
+    strncpy(msg, h->msg.c_str(), len - 1);
+    msg[len - 1] = 0;
+  }
+  return TLRB_OK;
+}
+
+int32_t tlrb_bessel_k(double nu, const double* x, int64_t count, double* out, int32_t device) {
+  if (!x || !out || count < 0 || !(nu > 0 && nu <= 5)) return TLRB_ERR_ARG;
+  return guarded(nullptr, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(device));
+    double *dxp, *dop;
+    TLRB_CUDA(cudaMalloc(&dxp, std::max<int64_t>(1, count) * 8));
+    TLRB_CUDA(cudaMalloc(&dop, std::max<int64_t>(1, count) * 8));
+    TLRB_CUDA(cudaMemcpy(dxp, x, count * 8, cudaMemcpyHostToDevice));
+    if (count) launch_bessel(nu, dxp, dop, count, 0);
+    TLRB_CUDA(cudaMemcpy(out, dop, count * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dxp);
+    cudaFree(dop);
+    return TLRB_OK;
+  });
+}
+
+int32_t tlrb_matern_block(const double* rows_xy, int64_t m, const double* cols_xy, int64_t n, double th1,
+                          double th2, double th3, double* out, int32_t device) {
+  if (!rows_xy || !cols_xy || !out || m < 1 || n < 1) return TLRB_ERR_ARG;
+  if (validate(th1, th2, th3, 0.0, 0.0)) return TLRB_ERR_ARG;
+  return guarded(nullptr, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(device));
+    std::vector<double> xs(m + n), ys(m + n);
+    for (int64_t i = 0; i < m; ++i) { xs[i] = rows_xy[2 * i]; ys[i] = rows_xy[2 * i + 1]; }
+    for (int64_t i = 0; i < n; ++i) { xs[m + i] = cols_xy[2 * i]; ys[m + i] = cols_xy[2 * i + 1]; }
+    double *px, *py, *po;
+    TLRB_CUDA(cudaMalloc(&px, (m + n) * 8));
+    TLRB_CUDA(cudaMalloc(&py, (m + n) * 8));
+    TLRB_CUDA(cudaMalloc(&po, m * n * 8));
+    TLRB_CUDA(cudaMemcpy(px, xs.data(), (m + n) * 8, cudaMemcpyHostToDevice));
+    TLRB_CUDA(cudaMemcpy(py, ys.data(), (m + n) * 8, cudaMemcpyHostToDevice));
+    DescArena ar;
+    ar.init(1 << 20);
+    // diag_add applies where global row == global col: rows and cols are disjoint index ranges here
+    launch_gen_tiles({GenTile{po, (int)m, 0, (int)m, (int)m, (int)n, 0.0}}, px, py, make_matern(th1, th2, th3),
+                     ar, 0);
+    TLRB_CUDA(cudaMemcpy(out, po, m * n * 8, cudaMemcpyDeviceToHost));
+    ar.release();
+    cudaFree(px);
+    cudaFree(py);
+    cudaFree(po);
+    return TLRB_OK;
+  });
+}
+
+int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc, int32_t* rank, double* u,
+                           double* v, int32_t device) {
+  if (!a || !rank || m < 1 || n < 1 || !(acc > 0 && acc < 1)) return TLRB_ERR_ARG;
+  // a one-tile handle: nb = max(m, n), compression workspace of one job
+  std::vector<double> xy(2 * (size_t)std::max(m, n), 0.0);
+  for (size_t i = 0; i < xy.size() / 2; ++i) xy[2 * i] = (double)i;
+  int32_t err = 0;
+  tlrb_handle* h = tlrb_create(xy.data(), std::max(m, n), std::max(m, n), 1, 0, device, &err);
+  if (!h) return err;
+  const int rc = guarded(h, [&]() -> int {
+    Job J{};
+    bind_slot(h, J, 0);
+    J.m = m;
+    J.n = n;
+    J.s = std::min(n, 64);
+    J.kind = 0;
+    J.Uout = h->diag;  // the diag arena (nb x nb) receives U (m x k)
+    double* dv;
+    TLRB_CUDA(cudaMalloc(&dv, (size_t)n * std::min(m, n) * 8));
+    J.Vout = dv;
+    J.ldu = m;
+    J.ldv = n;
+    J.seed = 99;
+    TLRB_CUDA(cudaMemcpy(J.M, a, (size_t)m * n * 8, cudaMemcpyHostToDevice));
+    std::vector<Job> jobs{J};
+    compress_jobs(h, jobs, acc);
+    h->sync();
+    const int k = jobs[0].out_rank;
+    *rank = k;
+    if (u && k) TLRB_CUDA(cudaMemcpy(u, h->diag, (size_t)m * k * 8, cudaMemcpyDeviceToHost));
+    if (v && k) TLRB_CUDA(cudaMemcpy(v, dv, (size_t)n * k * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dv);
+    return TLRB_OK;
+  });
+  tlrb_destroy(h);
+  return rc;
+}
+
+int64_t tlrb_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+"""Parity of the CUDA path (through libtlrb200.so's C ABI) with the reference
+goldens and the CPU oracle.  Tolerances (BASELINE.json north_star):
+dense log-likelihood 1e-10 relative; TLR within max(1e-8, 10*acc) relative
+of the reference TLR at the same accuracy."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GOLD
+from oracle import tlr_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["s120", "s300", "s300nu", "s500r", "C1"]
+
+
+def test_bessel_device(tb):
+    g = np.load(GOLD / "bessel.npz")
+    for i, nu in enumerate(g["nus"]):
+        got = tb.bessel_k(float(nu), g["xs"])
+        np.testing.assert_allclose(got, g["kv"][i], rtol=1e-13, atol=0)
+
+
+def test_matern_block_device(tb):
+    g = np.load(GOLD / "tiles.npz")
+    for key in [k for k in g.files if k.endswith("_exact")]:
+        n, seed, nu = key.split("_")[:3]
+        th = {"0.5": (1.0, 0.1, 0.5), "1.7": (1.3, 0.05, 1.7), "2.5": (0.7, 0.2, 2.5)}[nu]
+        xy = orc.generate_locations(int(n), int(seed))
+        a = tb.matern_block(xy[: int(n) // 2], xy[int(n) // 2:], tb.MaternParams(*th))
+        ref = g[key][: int(n) // 2, int(n) // 2:]
+        np.testing.assert_allclose(a, ref, rtol=1e-13, atol=1e-16)
+
+
+def test_compress_tile_ranks_device(tb):
+    g = np.load(GOLD / "compression.npz")
+    for i, j in [(1, 0), (2, 0), (3, 0), (3, 2)]:
+        tile = g[f"tile_{i}_{j}"]
+        nrm = np.linalg.norm(tile)
+        for eps in (1e-5, 1e-7, 1e-9, 1e-12):
+            u, v = tb.compress_tile(tile, eps)
+            assert u.shape[1] == int(g[f"rank_{i}_{j}_{eps:g}"]), (i, j, eps, u.shape[1])
+            err = np.linalg.norm(tile - u @ v.T)
+            assert err <= eps * nrm * (1 + 1e-6), (i, j, eps, err / (eps * nrm))
+
+
+def test_compress_edge_cases_device(tb):
+    z = np.zeros((40, 30))
+    u, v = tb.compress_tile(z, 1e-6)
+    assert u.shape[1] == 0
+    a = np.outer(np.arange(1.0, 41.0), np.linspace(-1, 1, 30))
+    u, v = tb.compress_tile(a, 1e-9)
+    assert u.shape[1] == 1
+    np.testing.assert_allclose(u @ v.T, a, atol=1e-12 * np.abs(a).max())
+
+
+@pytest.mark.parametrize("name", CASES + ["C2"])
+def test_loglik_dense_parity(tb, gold, name):
+    if name not in gold["loglik"]:
+        pytest.skip("C2 goldens not generated")
+    e = gold["loglik"][name]
+    locs = tb.generate_locations(e["n"], e["loc_seed"])
+    th = e["theta"]
+    p = tb.MaternParams(*th)
+    r = e["modes"]["dense"]
+    ll, ld, q, st = tb.log_likelihood_parts(locs, gold["z"][name], p, tb.LikelihoodConfig(nb=e["nb"]))
+    assert abs(ll - r["ll"]) <= 1e-10 * abs(r["ll"]), (ll, r["ll"])
+    assert abs(ld - r["log_det"]) <= 1e-9 * max(1.0, abs(r["log_det"]))
+    assert st["kernel_launches"] > 0
+
+
+@pytest.mark.parametrize("name", CASES + ["C2"])
+def test_loglik_tlr_parity(tb, gold, name):
+    if name not in gold["loglik"]:
+        pytest.skip("C2 goldens not generated")
+    e = gold["loglik"][name]
+    locs = tb.generate_locations(e["n"], e["loc_seed"])
+    p = tb.MaternParams(*e["theta"])
+    for mode, r in e["modes"].items():
+        if mode == "dense":
+            continue
+        acc = float(mode.split(":")[1])
+        cfg = tb.LikelihoodConfig(mode="tlr", accuracy=acc, nb=e["nb"])
+        ll, ld, q, st = tb.log_likelihood_parts(locs, gold["z"][name], p, cfg)
+        tol = max(1e-8, 10 * acc)
+        assert abs(ll - r["ll"]) <= tol * abs(r["ll"]), (mode, ll, r["ll"], abs(ll - r["ll"]) / abs(r["ll"]))
+        if r.get("factor_ranks"):
+            h = tb.api._handle_for(locs.coords, min(e["nb"], e["n"]), None, 1)
+            rm = h.rank_map()
+            ref = r["factor_ranks"]
+            diff = sum(1 for k, v in ref.items() if rm[tuple(map(int, k.split(",")))] != v)
+            assert diff <= max(1, len(ref) // 50), f"{diff} of {len(ref)} factor ranks differ"
+
+
+def test_solves_device(tb):
+    g = np.load(GOLD / "solves.npz")
+    for n, nb, eps in [(120, 40, 1e-9), (150, 32, 1e-7), (200, 64, 1e-12)]:
+        key = f"{n}_{nb}_{eps:g}"
+        locs = tb.generate_locations(n, 33)
+        p = tb.MaternParams(1.0, 0.1, 0.5)
+        rhs = g[key + "_rhs"]
+        for acc, tag in ((None, "dense"), (eps, "tlr")):
+            h = tb.Handle(locs.coords, nb)
+            _, ld, _ = h.loglik(np.zeros(n), p, acc)
+            x = h.solve(rhs)
+            ref = g[f"{key}_{tag}_x"]
+            rel = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+            assert rel <= (1e-9 if acc is None else max(1e-8, 1000 * eps)), (key, tag, rel)
+            assert ld == pytest.approx(float(g[f"{key}_{tag}_logdet"]), rel=1e-10 if acc is None else 100 * eps)
+            h.close()
+
+
+def test_kriging_device(tb):
+    g = np.load(GOLD / "kriging.npz")
+    p = tb.MaternParams(1.0, 0.1, 0.5)
+    known, unknown = tb.LocationSet(g["known"]), tb.LocationSet(g["unknown"])
+    pred = tb.predict(tb.PredictionProblem(known, g["z"], unknown, p, nb=100))
+    np.testing.assert_allclose(pred, g["dense_nb100"], rtol=1e-10, atol=1e-12)
+    pred = tb.predict(tb.PredictionProblem(known, g["z"], unknown, p, "tlr", 1e-9, 100))
+    assert np.max(np.abs(pred - g["tlr9_nb100"])) <= 1e-8
+
+
+def test_kriging_exact_interpolation(tb):
+    # test_predict.py:30-37: an unknown at a known site reproduces its value
+    g = np.load(GOLD / "kriging.npz")
+    locs = tb.LocationSet(g["interp_locs"])
+    z = g["interp_z"]
+    unknown = tb.LocationSet(g["interp_locs"][[5, 77, 300]])
+    pred = tb.predict(tb.PredictionProblem(locs, z, unknown, tb.MaternParams(1.0, 0.1, 0.5)))
+    np.testing.assert_allclose(pred, z[[5, 77, 300]], rtol=1e-10)
+
+
+def test_kriging_c1_holdout(tb):
+    g = np.load(GOLD / "kriging.npz")
+    locs = tb.generate_locations(1600, 0)
+    z = np.load(GOLD / "z.npz")["C1"]
+    mask = np.zeros(1600, bool)
+    mask[g["c1_holdout_idx"]] = True
+    p = tb.MaternParams(1.0, 0.1, 0.5)
+    kn, un = tb.LocationSet(locs.coords[~mask]), tb.LocationSet(locs.coords[mask])
+    pd = tb.predict(tb.PredictionProblem(kn, z[~mask], un, p, "dense", None, 400))
+    np.testing.assert_allclose(pd, g["c1_dense"], rtol=1e-9, atol=1e-11)
+    pt = tb.predict(tb.PredictionProblem(kn, z[~mask], un, p, "tlr", 1e-9, 400))
+    assert np.linalg.norm(pt - g["c1_tlr9"]) <= 1e-8 * np.linalg.norm(g["c1_tlr9"])
+
+
+def test_single_point_loglik(tb):
+    # test_stats.py:30-42
+    locs = tb.LocationSet(np.array([[0.0, 0.0]]))
+    p = tb.MaternParams(1.0, 0.001, 0.5)
+    assert tb.log_likelihood(locs, np.array([0.0]), p) == pytest.approx(-0.5 * math.log(2 * math.pi), rel=1e-12)
+    assert tb.log_likelihood(locs, np.array([1.0]), p) == pytest.approx(-1.4189385332046727, rel=1e-12)
+
+
+def test_npd_raises_with_tile(tb):
+    # test_linalg.py:121-127: smooth long-range kernel without nugget
+    locs = tb.generate_locations(120, 3)
+    p = tb.MaternParams(1.0, 2.0, 4.9)
+    with pytest.raises(tb.NotPositiveDefiniteError) as exc:
+        tb.log_likelihood(locs, np.zeros(120), p, tb.LikelihoodConfig(nb=48))
+    xy = locs.coords
+    with pytest.raises(orc.NotPositiveDefiniteError) as ref:
+        orc.log_likelihood(xy, np.zeros(120), (1.0, 2.0, 4.9), 48, None)
+    assert exc.value.tile_index == ref.value.tile_index
+
+
+def test_invalid_args(tb):
+    locs = tb.generate_locations(50, 1)
+    with pytest.raises(ValueError):
+        tb.log_likelihood(locs, np.zeros(49), tb.MaternParams(1.0, 0.1, 0.5))
+
+
+def test_permutation_invariance_dense(tb):
+    # test_stats.py:54-63
+    locs = tb.generate_locations(150, 14)
+    p = tb.MaternParams(1.0, 0.1, 0.8)
+    z = np.random.default_rng(3).standard_normal(150)
+    perm = np.random.default_rng(20240817).permutation(150)
+    l1 = tb.log_likelihood(locs, z, p, tb.LikelihoodConfig(nb=40))
+    l2 = tb.log_likelihood(tb.LocationSet(locs.coords[perm]), z[perm], p, tb.LikelihoodConfig(nb=40))
+    assert l2 == pytest.approx(l1, rel=1e-10)
+
+
+def test_deterministic(tb):
+    locs = tb.generate_locations(300, 8)
+    p = tb.MaternParams(1.0, 0.1, 0.5)
+    z = np.random.default_rng(5).standard_normal(300)
+    cfg = tb.LikelihoodConfig(mode="tlr", accuracy=1e-7, nb=64)
+    assert tb.log_likelihood(locs, z, p, cfg) == tb.log_likelihood(locs, z, p, cfg)
