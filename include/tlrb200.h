@@ -41,7 +41,8 @@ typedef struct tlrb_stats {
   double ms_compress;     /* initial compression only */
   double ms_factor;       /* tile Cholesky */
   double ms_solve;        /* forward solve + dot + log-det reduction */
-  double ms_total;
+  double ms_total;        /* host wall clock of the call */
+  double ms_device;       /* CUDA events on the handle's stream, call entry -> result ready */
   double flops;           /* algorithmic FP64 flops (SURVEY 8(d) formulas) */
   double bytes;           /* algorithmic HBM bytes (SURVEY 8(d) formulas) */
   int64_t stored_reals;   /* footprint() semantics, tilestore.py:150-163 */
@@ -113,6 +114,13 @@ int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc,
 
 /* Number of kernels this library has launched in this process. */
 int64_t tlrb_launch_count(void);
+
+/* Per-kernel-class profiler: CUDA events around every launch on its stream,
+ * plus the algorithmic flops / bytes of each launch.
+ * enable resets the counters.  Classes: 0..10 (name returned). */
+int32_t tlrb_profile_enable(int32_t on);
+int32_t tlrb_profile_read(int32_t cls, char* name, int32_t len, double* ms, double* flops,
+                          double* bytes, int64_t* launches);
 
 #ifdef __cplusplus
 }

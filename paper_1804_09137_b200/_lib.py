@@ -24,6 +24,7 @@ class TlrbStats(C.Structure):
         ("ms_factor", C.c_double),
         ("ms_solve", C.c_double),
         ("ms_total", C.c_double),
+        ("ms_device", C.c_double),
         ("flops", C.c_double),
         ("bytes", C.c_double),
         ("stored_reals", C.c_int64),
@@ -60,6 +61,9 @@ SIGNATURES = [
                                       C.c_double, _DP, C.c_int32]),
     ("tlrb_compress_tile", C.c_int32, [_DP, C.c_int32, C.c_int32, C.c_double, _IP, _DP, _DP, C.c_int32]),
     ("tlrb_launch_count", C.c_int64, []),
+    ("tlrb_profile_enable", C.c_int32, [C.c_int32]),
+    ("tlrb_profile_read", C.c_int32, [C.c_int32, C.c_char_p, C.c_int32, _DP, _DP, _DP,
+                                      C.POINTER(C.c_int64)]),
 ]
 
 
@@ -79,6 +83,24 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def profile_enable(on: bool = True):
+    load().tlrb_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel class: {ms, flops, bytes, launches}} since profile_enable()."""
+    lib = load()
+    out = {}
+    for cls in range(11):
+        name = C.create_string_buffer(64)
+        v = np.zeros(3)
+        cnt = C.c_int64(0)
+        lib.tlrb_profile_read(cls, name, 64, dptr(v[0:]), dptr(v[1:]), dptr(v[2:]), C.byref(cnt))
+        out[name.value.decode()] = {"ms": float(v[0]), "flops": float(v[1]), "bytes": float(v[2]),
+                                    "launches": int(cnt.value)}
+    return out
 
 
 def dptr(a: np.ndarray):

@@ -32,6 +32,35 @@ inline void post_launch() {
   if (e != cudaSuccess) throw CudaError(e, "kernel launch", __FILE__, __LINE__);
 }
 
+// ---- per-kernel-class profiler (CUDA events on the launching stream) ----
+enum KClass { K_GEN = 0, K_GEMM, K_TRSM, K_POTRF, K_QR, K_JACOBI, K_SUMSQ, K_COPY, K_GAUSS,
+              K_REDUCE, K_CROSS, K_NCLASS };
+extern const char* kclass_name[K_NCLASS];
+struct Profiler {
+  bool on = false;
+  double ms[K_NCLASS] = {}, flops[K_NCLASS] = {}, bytes[K_NCLASS] = {};
+  int64_t count[K_NCLASS] = {};
+  struct Pend { int cls; cudaEvent_t a, b; };
+  std::vector<Pend> pend;
+  std::vector<cudaEvent_t> pool;
+  int open_cls = -1;
+  cudaEvent_t open_ev = nullptr;
+  cudaEvent_t get();
+  void begin(int cls, cudaStream_t s);
+  void end(cudaStream_t s, double fl, double by);
+  void add_work(int cls, double fl, double by) { flops[cls] += fl; bytes[cls] += by; }
+  void drain();   // after a stream synchronisation
+  void reset();
+};
+extern Profiler g_prof;
+struct ProfScope {   // RAII: times one launch of class cls
+  cudaStream_t s; double fl, by;
+  ProfScope(int cls, cudaStream_t st, double f = 0, double b = 0) : s(st), fl(f), by(b) {
+    if (g_prof.on) g_prof.begin(cls, st);
+  }
+  ~ProfScope() { if (g_prof.on) g_prof.end(s, fl, by); }
+};
+
 // ------------------------------------------------------------------ Matern
 struct MaternParamsDev {
   double theta1, inv_theta2, nu, pref;   // pref = theta1 / (2^(nu-1) Gamma(nu))
@@ -86,7 +115,11 @@ struct JacobiProb {        // one-sided Jacobi on the columns of X (m x s)
 
 // ----------------------------------------------------------- small helpers
 struct SumsqProb { const double* A; int ld, m, n; double* out; };
-struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale; };
+// dst(r, c) = scale * (transpose ? src(c, r) : src(r, c)); tri: zero where r < c;
+// rowperm: dst row rowperm[r] receives row r
+struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale;
+                  int tri; const int* rowperm; };
+struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid_out; double stop_rel2; };
 struct GaussProb { double* A; int ld, m, n; uint64_t seed; };
 
 // Device-resident descriptor staging (pinned host ring -> device), reset at
@@ -114,6 +147,7 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
 void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);

@@ -147,6 +147,12 @@ void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t
   start.push_back(tot);
   const GemmProb* dp = ar.put(keep, s);
   const int* ds = ar.put(start, s);
+  double fl = 0, by = 0;
+  for (const GemmProb& p : keep) {
+    fl += 2.0 * p.m * p.n * p.k;
+    by += 8.0 * ((double)p.m * p.k + (double)p.k * p.n + (double)p.m * p.n * (p.beta != 0.0 ? 2 : 1));
+  }
+  ProfScope ps(K_GEMM, s, fl, by);
   dgemm_vbatch_kernel<<<tot, 128, 0, s>>>(dp, ds, (int)keep.size());
   post_launch();
 }

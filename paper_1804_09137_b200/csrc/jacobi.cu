@@ -9,17 +9,24 @@
 // part 2).  One-sided Jacobi is backward stable column by column and yields
 // exactly that.
 //
-// Layout: X (m x s, column-major, global/L2) holds the columns to be
-// orthogonalised (X = B^T of the range-finder, or M^T when unsketched).  One
-// CTA per matrix runs block-cyclic sweeps: block I (B columns) stays resident
-// in shared memory while blocks J > I stream through; every column pair is
-// rotated by one warp (dot products by lane-strided FMA + xor-shuffle
-// reduction).  After convergence the column norms are the singular values;
-// the columns are normalised, sorted descending and written to Vout, and the
-// truncation rank is computed from the sorted values plus the sketch
-// residual e2 (aux[0]).
+// Parallel layout: X (m x s, column-major) lives in global memory / L2 and is
+// cut into column blocks of B.  One thread-block CLUSTER (1..8 CTAs, sized by
+// the matrix) owns one matrix.  A sweep is a round-robin tournament over the
+// blocks: in each round the cluster's CTAs take disjoint block pairs (I, J),
+// stage both blocks in shared memory, rotate all B x B cross column pairs
+// (one warp per pair, B disjoint pairs per inner round) and write them back;
+// a cluster barrier separates rounds.  Pairs inside a block are rotated once
+// per sweep (round 0, where every block appears exactly once).  The sweep
+// loop stops when no pair of the whole cluster needed a rotation
+// (|a_p.a_q| <= m eps ||a_p|| ||a_q||, LAPACK dgesvj's tolerance).
+// Afterwards CTA 0 computes the column norms (= singular values), sorts them,
+// writes normalised columns in sorted order, and applies the truncation rule
+// with the sketch residual e2 (aux[0]) and the noise floor (aux[1]).
 #include "common.cuh"
 #include <cfloat>
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
 
 namespace tlrb {
 
@@ -29,8 +36,9 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// rotate columns a and b (length m, in shared memory); returns true if rotated
-__device__ __forceinline__ bool rotate_pair(double* a, double* b, int m, double tol, int lane) {
+// rotate columns a and b (length m, shared memory); true if rotated
+__device__ __forceinline__ bool rotate_pair(double* a, double* b, int m, double tol, double tiny2,
+                                            int lane) {
   double al = 0.0, be = 0.0, ga = 0.0;
   for (int r = lane; r < m; r += 32) {
     const double x = a[r], y = b[r];
@@ -41,7 +49,7 @@ __device__ __forceinline__ bool rotate_pair(double* a, double* b, int m, double 
   al = wsum(al);
   be = wsum(be);
   ga = wsum(ga);
-  if (ga == 0.0 || al == 0.0 || be == 0.0) return false;
+  if (ga == 0.0 || al <= tiny2 || be <= tiny2) return false;
   if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) return false;
   const double zeta = (be - al) / (2.0 * ga);
   const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
@@ -55,76 +63,118 @@ __device__ __forceinline__ bool rotate_pair(double* a, double* b, int m, double 
   return true;
 }
 
-__global__ void jacobi_kernel(const JacobiProb* __restrict__ probs, int B, int max_sweeps) {
+// round-robin tournament over nplayers (even): match idx of round r
+__device__ __forceinline__ void match(int r, int idx, int np, int& p, int& q) {
+  const int rot = np - 1;
+  if (idx == 0) {
+    p = r % rot;
+    q = np - 1;
+  } else {
+    p = (r + idx) % rot;
+    q = (r - idx + rot) % rot;
+  }
+}
+
+__global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
+                                                             int max_sweeps) {
   extern __shared__ double sm[];
-  const JacobiProb P = probs[blockIdx.x];
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const JacobiProb P = probs[blockIdx.x / CL];
   const int m = P.m, s = P.s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nthr = blockDim.x;
   double* S0 = sm;
   double* S1 = sm + (size_t)B * m;
-  __shared__ int rotated;
-  const double tol = sqrt((double)m) * DBL_EPSILON;
+  __shared__ int rot_flag;
+  // rotation tolerance: LAPACK dgesvj's m*eps, tightened for very small acc
+  // (the truncated product M V V^T inherits the columns' non-orthogonality);
+  // columns below tau*||M|| carry no information for the truncation at acc
+  // (their energy is preserved by the rotations) and are not rotated.
+  const double tol = fmin((double)m * DBL_EPSILON, fmax(0.01 * P.eps, 2.0 * sqrt((double)m) * DBL_EPSILON));
+  const double tau = fmax(1e-3 * P.eps, 2.0 * sqrt((double)m) * DBL_EPSILON);
+  const double tiny2 = tau * tau * P.aux[2];
   const int nblk = (s + B - 1) / B;
+  const int np = nblk + (nblk & 1);   // pad with a dummy block
   int sweeps = 0;
 
   auto load = [&](double* dst, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     for (int e = threadIdx.x; e < m * B; e += nthr) {
       const int r = e % m, c = e / m;
-      dst[c * m + r] = (c < nc) ? P.X[(size_t)(c0 + c) * P.ldx + r] : 0.0;
+      dst[c * m + r] = (c < nc) ? __ldcg(P.X + (size_t)(c0 + c) * P.ldx + r) : 0.0;
     }
   };
   auto store = [&](const double* src, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     for (int e = threadIdx.x; e < m * nc; e += nthr) {
       const int r = e % m, c = e / m;
-      P.X[(size_t)(c0 + c) * P.ldx + r] = src[c * m + r];
+      __stcg(P.X + (size_t)(c0 + c) * P.ldx + r, src[c * m + r]);
+    }
+  };
+  auto within = [&](double* S, int nc, bool& any) {   // all pairs inside one block
+    for (int r = 0; r < B - 1; ++r) {
+      if (warp < B / 2) {
+        int p, q;
+        match(r, warp, B, p, q);
+        if (p < nc && q < nc) any |= rotate_pair(S + p * m, S + q * m, m, tol, tiny2, lane);
+      }
+      __syncthreads();
     }
   };
 
   if (s > 1) {
     for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
-      if (threadIdx.x == 0) rotated = 0;
-      __syncthreads();
       bool any = false;
-      for (int I = 0; I < nblk; ++I) {
-        load(S0, I);
-        __syncthreads();
-        const int ncI = min(B, s - I * B);
-        // pairs inside block I: round-robin tournament, B-1 rounds of B/2 pairs
-        for (int r = 0; r < B - 1; ++r) {
-          if (warp < B / 2) {
-            int p, q;
-            if (warp == 0) { p = r; q = B - 1; }
-            else { p = (r + warp) % (B - 1); q = (r - warp + (B - 1)) % (B - 1); }
-            if (p < ncI && q < ncI) any |= rotate_pair(S0 + p * m, S0 + q * m, m, tol, lane);
+      for (int r = 0; r < np - 1; ++r) {
+        for (int idx = crank; idx < np / 2; idx += CL) {
+          int I, J;
+          match(r, idx, np, I, J);
+          if (I >= nblk) { const int t = I; I = J; J = t; }   // I real, J maybe dummy
+          const bool realJ = J < nblk;
+          load(S0, I);
+          if (realJ) load(S1, J);
+          __syncthreads();
+          const int ncI = min(B, s - I * B);
+          const int ncJ = realJ ? min(B, s - J * B) : 0;
+          if (r == 0) {
+            within(S0, ncI, any);
+            if (realJ) within(S1, ncJ, any);
           }
-          __syncthreads();
-        }
-        for (int J = I + 1; J < nblk; ++J) {
-          load(S1, J);
-          __syncthreads();
-          const int ncJ = min(B, s - J * B);
-          for (int r = 0; r < B; ++r) {
-            if (warp < B) {
-              const int p = warp, q = (warp + r) % B;
-              if (p < ncI && q < ncJ) any |= rotate_pair(S0 + p * m, S1 + q * m, m, tol, lane);
+          if (realJ) {
+            for (int rr = 0; rr < B; ++rr) {
+              if (warp < B) {
+                const int p = warp, q = (warp + rr) % B;
+                if (p < ncI && q < ncJ) any |= rotate_pair(S0 + p * m, S1 + q * m, m, tol, tiny2, lane);
+              }
+              __syncthreads();
             }
-            __syncthreads();
           }
-          store(S1, J);
+          store(S0, I);
+          if (realJ) store(S1, J);
           __syncthreads();
         }
-        store(S0, I);
-        __syncthreads();
+        __threadfence();
+        cl.sync();
       }
-      if (any && lane == 0) rotated = 1;
+      // cluster-wide convergence decision through distributed shared memory
+      if (threadIdx.x == 0) rot_flag = 0;
       __syncthreads();
-      if (!rotated) break;
+      if (any && lane == 0) atomicOr(&rot_flag, 1);
+      cl.sync();
+      int total = 0;
+      if (threadIdx.x == 0)
+        for (int c = 0; c < CL; ++c) total |= *cl.map_shared_rank(&rot_flag, c);
       __syncthreads();
+      if (threadIdx.x == 0) S0[0] = (double)total;   // broadcast via smem (S0 is free here)
+      __syncthreads();
+      const bool more = S0[0] != 0.0;
+      cl.sync();   // everyone has read the flags before they are reset
+      if (!more) break;
     }
   }
+  if (crank != 0) return;
   if (threadIdx.x == 0) *P.sweeps_out = sweeps;
 
   // ---- singular values = column norms; sort descending; normalise
@@ -133,7 +183,7 @@ __global__ void jacobi_kernel(const JacobiProb* __restrict__ probs, int B, int m
   for (int c = warp; c < s; c += nw) {
     double a = 0.0;
     for (int r = lane; r < m; r += 32) {
-      const double x = P.X[(size_t)c * P.ldx + r];
+      const double x = __ldcg(P.X + (size_t)c * P.ldx + r);
       a = fma(x, x, a);
     }
     a = wsum(a);
@@ -155,7 +205,7 @@ __global__ void jacobi_kernel(const JacobiProb* __restrict__ probs, int B, int m
     const double v = sig[c];
     const double inv = v > 0.0 ? 1.0 / v : 0.0;
     for (int r = lane; r < m; r += 32)
-      P.Vout[(size_t)pos * P.ldv + r] = P.X[(size_t)c * P.ldx + r] * inv;
+      P.Vout[(size_t)pos * P.ldv + r] = __ldcg(P.X + (size_t)c * P.ldx + r) * inv;
     if (lane == 0) P.sigma[pos] = v;
   }
   __syncthreads();
@@ -182,19 +232,45 @@ __global__ void jacobi_kernel(const JacobiProb* __restrict__ probs, int B, int m
 
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
-  int mmax = 1, smax = 1;
-  for (const JacobiProb& p : probs) {
-    mmax = std::max(mmax, p.m);
-    smax = std::max(smax, p.s);
-  }
+  int mmax = 1;
+  for (const JacobiProb& p : probs) mmax = std::max(mmax, p.m);
   int B = 16;
   while (B > 2 && (size_t)2 * B * mmax * 8 > 200 * 1024) B >>= 1;
-  size_t smem = std::max((size_t)2 * B * mmax * 8, (size_t)smax * 12 + 64);
-  TLRB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  const JacobiProb* dp = ar.put(probs, s);
-  jacobi_kernel<<<(unsigned)probs.size(), 32 * B, smem, s>>>(dp, B, 60);
-  post_launch();
+  // group by cluster size: one CTA per block pair of a round, at most 8
+  std::vector<JacobiProb> groups[4];
+  for (const JacobiProb& p : probs) {
+    const int nblk = (p.s + B - 1) / B;
+    const int pairs = (nblk + 1) / 2;
+    const int g = pairs <= 1 ? 0 : pairs <= 2 ? 1 : pairs <= 4 ? 2 : 3;
+    groups[g].push_back(p);
+  }
+  for (int g = 0; g < 4; ++g) {
+    if (groups[g].empty()) continue;
+    const int CL = 1 << g;
+    int smax = 1;
+    for (const JacobiProb& p : groups[g]) smax = std::max(smax, p.s);
+    const size_t smem = std::max((size_t)2 * B * mmax * 8, (size_t)smax * 12 + 64);
+    TLRB_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    const JacobiProb* dp = ar.put(groups[g], s);
+    double by = 0;
+    for (const JacobiProb& p : groups[g]) by += 8.0 * 3.0 * p.m * p.s;
+    ProfScope ps(K_JACOBI, s, 0, by);  // flops added once the sweep counts are known
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(groups[g].size() * CL));
+    cfg.blockDim = dim3(32 * B);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TLRB_CUDA(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, dp, B, 60));
+    post_launch();
+  }
 }
 
 }  // namespace tlrb

@@ -180,6 +180,9 @@ void launch_gen_tiles(const std::vector<GenTile>& tiles, const double* x, const 
   if (tot == 0) return;
   const GenTile* dt = ar.put(tiles, s);
   const int* ds = ar.put(start, s);
+  double by = 0;
+  for (const GenTile& t : tiles) by += 8.0 * t.m * t.n;
+  ProfScope ps(K_GEN, s, 0, by);
   gen_tiles_kernel<<<tot, 256, 0, s>>>(dt, ds, (int)tiles.size(), x, y, p);
   post_launch();
 }
@@ -240,6 +243,7 @@ void launch_cross_gemv(const double* kx, const double* ky, const double* w, int6
                        double* partial, double* out, cudaStream_t s) {
   const int nchunk = (int)((n + XG_CHUNK - 1) / XG_CHUNK);
   dim3 grid(nchunk, (unsigned)m);
+  ProfScope ps(K_CROSS, s, 2.0 * n * m, 24.0 * n);
   cross_gemv_kernel<<<grid, 256, 0, s>>>(kx, ky, w, n, ux, uy, p, partial);
   post_launch();
   row_sum_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(partial, nchunk, m, out);

@@ -7,6 +7,49 @@
 namespace tlrb {
 
 int64_t g_launches = 0;
+Profiler g_prof;
+const char* kclass_name[K_NCLASS] = {"gen_tiles", "dgemm_vbatch", "trsm_vbatch", "potrf_block",
+                                     "qr_householder", "jacobi_svd", "sumsq", "copy", "gaussian",
+                                     "reduce", "cross_gemv"};
+
+cudaEvent_t Profiler::get() {
+  if (pool.empty()) {
+    cudaEvent_t e;
+    TLRB_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = pool.back();
+  pool.pop_back();
+  return e;
+}
+void Profiler::begin(int cls, cudaStream_t s) {
+  open_cls = cls;
+  open_ev = get();
+  TLRB_CUDA(cudaEventRecord(open_ev, s));
+}
+void Profiler::end(cudaStream_t s, double fl, double by) {
+  if (open_cls < 0) return;
+  cudaEvent_t b = get();
+  TLRB_CUDA(cudaEventRecord(b, s));
+  pend.push_back({open_cls, open_ev, b});
+  flops[open_cls] += fl;
+  bytes[open_cls] += by;
+  count[open_cls] += 1;
+  open_cls = -1;
+}
+void Profiler::drain() {
+  for (const Pend& p : pend) {
+    float a = 0;
+    if (cudaEventElapsedTime(&a, p.a, p.b) == cudaSuccess) ms[p.cls] += a;
+    pool.push_back(p.a);
+    pool.push_back(p.b);
+  }
+  pend.clear();
+}
+void Profiler::reset() {
+  drain();
+  for (int i = 0; i < K_NCLASS; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0;
+}
 
 void DescArena::init(size_t bytes) {
   TLRB_CUDA(cudaHostAlloc(&h_, bytes, cudaHostAllocDefault));
@@ -57,6 +100,9 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const SumsqProb* __restrict_
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
   const SumsqProb* dp = ar.put(probs, s);
+  double by = 0;
+  for (const SumsqProb& p : probs) by += 8.0 * p.m * p.n;
+  ProfScope ps(K_SUMSQ, s, 2.0 * by / 8, by);
   sumsq_kernel<<<(unsigned)probs.size(), 256, 0, s>>>(dp);
   post_launch();
 }
@@ -70,8 +116,10 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyProb* __restrict__ 
   const int64_t e0 = part * per, e1 = min(tot, e0 + per);
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const int r = (int)(e % P.m), c = (int)(e / P.m);
-    const double v = P.transpose ? P.src[(size_t)r * P.lds + c] : P.src[(size_t)c * P.lds + r];
-    P.dst[(size_t)c * P.ldd + r] = P.scale * v;
+    double v = P.transpose ? P.src[(size_t)r * P.lds + c] : P.src[(size_t)c * P.lds + r];
+    if (P.tri && r < c) v = 0.0;
+    const int rd = P.rowperm ? P.rowperm[r] : r;
+    P.dst[(size_t)c * P.ldd + rd] = P.scale * v;
   }
 }
 
@@ -86,6 +134,9 @@ void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t
   if (keep.empty()) return;
   const int chunks = (int)std::min<int64_t>(64, (mx + 8191) / 8192);
   const CopyProb* dp = ar.put(keep, s);
+  double by = 0;
+  for (const CopyProb& p : keep) by += 16.0 * p.m * p.n;
+  ProfScope ps(K_COPY, s, 0, by);
   copy_kernel<<<(unsigned)(keep.size() * chunks), 256, 0, s>>>(dp, chunks);
   post_launch();
 }
@@ -115,6 +166,9 @@ __global__ void __launch_bounds__(256) gaussian_kernel(const GaussProb* __restri
 void launch_gaussian(const std::vector<GaussProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
   const GaussProb* dp = ar.put(probs, s);
+  double by = 0;
+  for (const GaussProb& p : probs) by += 8.0 * p.m * p.n;
+  ProfScope ps(K_GAUSS, s, 0, by);
   dim3 grid(16, (unsigned)probs.size());
   gaussian_kernel<<<grid, 256, 0, s>>>(dp);
   post_launch();
@@ -139,17 +193,19 @@ __global__ void __launch_bounds__(1024) reduce_kernel(const double* x, int n, do
 }
 
 void launch_sum_log(const double* logdiag, int n, double* out, cudaStream_t s) {
+  ProfScope ps(K_REDUCE, s, n, 8.0 * n);
   reduce_kernel<<<1, 1024, 0, s>>>(logdiag, n, out, 0);
   post_launch();
 }
 void launch_dot(const double* x, int n, double* out, cudaStream_t s) {
+  ProfScope ps(K_REDUCE, s, 2.0 * n, 8.0 * n);
   reduce_kernel<<<1, 1024, 0, s>>>(x, n, out, 1);
   post_launch();
 }
 
 // ------------------------------------------------ compression bookkeeping
 // sums[6p + {0..5}] = {||M||^2, e2, ||U1||^2, ||U2||^2, ||V1||^2, ||V2||^2}
-// aux[2p] = e2 (0 when unsketched), aux[2p+1] = noise floor
+// aux[3p] = e2 (0 when unsketched), aux[3p+1] = noise floor, aux[3p+2] = ||M||^2
 //   50 eps_mach ||[U1 U2]||_F ||[V1 V2]||_F  (compression.py:78), 0 for tiles;
 // ok[p] = e2 <= rel_tol2 ||M||^2.
 __global__ void aux_kernel(const double* sums, const int* kinds, int nprob, double* aux, int* ok,
@@ -159,8 +215,9 @@ __global__ void aux_kernel(const double* sums, const int* kinds, int nprob, doub
   const double* S = sums + 6 * p;
   const int kind = kinds[p];   // bit0: sketched, bit1: recompression
   const double e2 = (kind & 1) ? S[1] : 0.0;
-  aux[2 * p] = e2;
-  aux[2 * p + 1] = (kind & 2) ? 50.0 * DBL_EPSILON * sqrt(S[2] + S[3]) * sqrt(S[4] + S[5]) : 0.0;
+  aux[3 * p] = e2;
+  aux[3 * p + 1] = (kind & 2) ? 50.0 * DBL_EPSILON * sqrt(S[2] + S[3]) * sqrt(S[4] + S[5]) : 0.0;
+  aux[3 * p + 2] = S[0];
   ok[p] = (!(kind & 1)) || (e2 <= rel_tol2 * S[0]);
 }
 

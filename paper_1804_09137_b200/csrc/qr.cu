@@ -198,6 +198,13 @@ void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s) 
   TLRB_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
   const QrProb* dp = ar.put(probs, s);
+  double fl = 0, by = 0;
+  for (const QrProb& p : probs) {
+    const double m = p.m, k = std::min(p.m, p.s);
+    fl += 2.0 * (2.0 * m * k * k - 2.0 / 3.0 * k * k * k);  // geqrf + orgqr
+    by += 8.0 * (2.0 * m * p.s);
+  }
+  ProfScope ps(K_QR, s, fl, by);
   qr_kernel<<<(unsigned)probs.size(), 512, smem, s>>>(dp, cf);
   post_launch();
 }

@@ -78,6 +78,7 @@ struct tlrb_handle {
   int* d_ok = nullptr;           // per job
   int* d_rank = nullptr;         // per job
   int* d_sweeps = nullptr;       // per job
+  int* d_perm = nullptr;         // nb per job (QRCP column permutation)
   // state
   int factor_mode = 0;           // 0: none, 1: dense, 2: tlr
   MaternParamsDev mp{};
@@ -95,6 +96,7 @@ struct tlrb_handle {
   void sync() {
     TLRB_CUDA(cudaStreamSynchronize(stream));
     ar.reset();
+    if (g_prof.on) g_prof.drain();
   }
 };
 
@@ -128,75 +130,51 @@ void bind_slot(tlrb_handle* h, Job& J, int slot) {
 
 // Compress the M of every job (already formed in its slot) to acc; writes
 // U = M V_k (m x k) and V_k (n x k) into the job's output slabs.
+//   1. E <- M (the original is needed for U = M V_k)
+//   2. truncated QRCP of M until ||residual||_F <= 1e-3 acc ||M||_F
+//   3. X = R^T (n x r, masked transpose), one-sided Jacobi on X -> sorted
+//      sigma, normalised columns (= right singular vectors in pivoted order),
+//      truncation rank k with e2 = ||residual||^2 and the noise floor
+//   4. V_k = P * columns (row un-permutation), U = E V_k (DMMA GEMM)
 void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   const int nj = (int)jobs.size();
   if (!nj) return;
   cudaStream_t s = h->stream;
-  {
-    std::vector<SumsqProb> sq;
-    for (int j = 0; j < nj; ++j) sq.push_back({jobs[j].M, jobs[j].m, jobs[j].m, jobs[j].n, h->d_sums + 6 * j});
-    launch_sumsq(sq, h->ar, s);
-  }
-  std::vector<int> kinds(nj), pending;
-  for (int j = 0; j < nj; ++j) {
-    Job& J = jobs[j];
-    if (J.s >= kFullSketchFrac * J.n) J.s = J.n;
-    if (J.s < J.n) pending.push_back(j);
-  }
-  int attempt = 0;
-  while (!pending.empty()) {
-    std::vector<GaussProb> gp;
-    std::vector<GemmProb> g1, g2, g3;
-    std::vector<QrProb> qp;
-    std::vector<SumsqProb> sq;
-    for (int j : pending) {
-      Job& J = jobs[j];
-      gp.push_back({J.Om, J.n, J.n, J.s, J.seed * 1000003ull + (uint64_t)attempt * 7919ull + 1});
-      g1.push_back({J.M, J.Om, nullptr, J.Y, J.m, J.s, J.n, J.m, J.n, J.m, J.m, 0, 0, 0, 1.0, 0.0});
-      qp.push_back({J.Y, J.m, J.Q, J.m, J.T, J.m, J.s});
-      g2.push_back({J.M, J.Q, nullptr, J.Bt, J.n, J.s, J.m, J.m, J.m, J.n, J.n, 1, 0, 0, 1.0, 0.0});
-      g3.push_back({J.Q, J.Bt, J.M, J.E, J.m, J.n, J.s, J.m, J.n, J.m, J.m, 0, 1, 0, -1.0, 1.0});
-      sq.push_back({J.E, J.m, J.m, J.n, h->d_sums + 6 * j + 1});
-    }
-    launch_gaussian(gp, h->ar, s);
-    launch_gemm(g1, h->ar, s);
-    launch_qr(qp, h->ar, s);
-    launch_gemm(g2, h->ar, s);
-    launch_gemm(g3, h->ar, s);
-    launch_sumsq(sq, h->ar, s);
-    for (int j = 0; j < nj; ++j) kinds[j] = (jobs[j].s < jobs[j].n ? 1 : 0) | jobs[j].kind;
-    TLRB_CUDA(cudaMemcpyAsync(h->d_kind, h->ar.put(kinds, s), nj * sizeof(int), cudaMemcpyDeviceToDevice, s));
-    launch_aux(h->d_sums, h->d_kind, nj, h->d_aux, h->d_ok, (kSketchRelTol * acc) * (kSketchRelTol * acc), s);
-    std::vector<int> ok(nj);
-    TLRB_CUDA(cudaMemcpyAsync(ok.data(), h->d_ok, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
-    h->sync();
-    std::vector<int> next;
-    for (int j : pending) {
-      if (ok[j]) continue;
-      Job& J = jobs[j];
-      ++h->retries;
-      J.s = std::min(J.n, 2 * J.s);
-      if (J.s >= kFullSketchFrac * J.n) J.s = J.n;
-      if (J.s < J.n) next.push_back(j);
-    }
-    pending.swap(next);
-    ++attempt;
-  }
-  // unsketched jobs: B^T = M^T
+  int* d_perm = reinterpret_cast<int*>(h->d_perm);
   {
     std::vector<CopyProb> cp;
-    for (Job& J : jobs)
-      if (J.s == J.n) { J.s = J.m; cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.m, 1, 1.0}); J.kind |= 4; }
+    std::vector<QrcpProb> qp;
+    for (int j = 0; j < nj; ++j) {
+      Job& J = jobs[j];
+      cp.push_back({J.M, J.m, J.E, J.m, J.m, J.n, 0, 1.0, 0, nullptr});
+      qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, h->d_rank + j, h->d_sums + 6 * j + 1,
+                    (kSketchRelTol * acc) * (kSketchRelTol * acc)});
+    }
+    launch_copy(cp, h->ar, s);
+    launch_qrcp(qp, h->ar, s);
+  }
+  std::vector<int> rr(nj);
+  TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  h->sync();
+  std::vector<int> kinds(nj);
+  {
+    std::vector<CopyProb> cp;
+    for (int j = 0; j < nj; ++j) {
+      Job& J = jobs[j];
+      J.s = rr[j];
+      kinds[j] = 1 | (J.kind & 2);   // e2 = QRCP residual (sums[6j+1])
+      // X (n x r): X(p, c) = R(c, p) for p >= c
+      if (J.s) cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.s, 1, 1.0, 1, nullptr});
+    }
     launch_copy(cp, h->ar, s);
   }
-  for (int j = 0; j < nj; ++j) kinds[j] = ((jobs[j].kind & 4) ? 0 : 1) | (jobs[j].kind & 2);
   TLRB_CUDA(cudaMemcpyAsync(h->d_kind, h->ar.put(kinds, s), nj * sizeof(int), cudaMemcpyDeviceToDevice, s));
   launch_aux(h->d_sums, h->d_kind, nj, h->d_aux, h->d_ok, 0.0, s);
   {
     std::vector<JacobiProb> jp;
     for (int j = 0; j < nj; ++j) {
       Job& J = jobs[j];
-      jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, h->d_aux + 2 * j, acc, h->d_rank + j,
+      jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, h->d_aux + 3 * j, acc, h->d_rank + j,
                     h->d_sweeps + j, J.n, J.s});
     }
     launch_jacobi(jp, h->ar, s);
@@ -209,15 +187,18 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   std::vector<CopyProb> cv;
   for (int j = 0; j < nj; ++j) {
     Job& J = jobs[j];
-    J.out_rank = rk[j];
-    h->max_sweeps = std::max(h->max_sweeps, sw[j]);
-    if (rk[j] > h->cap) throw CudaError(cudaErrorMemoryAllocation, "tile rank exceeds max_rank capacity", __FILE__, __LINE__);
-    if (!rk[j]) continue;
-    gu.push_back({J.M, J.Vs, nullptr, J.Uout, J.m, rk[j], J.n, J.m, J.n, J.ldu, J.ldu, 0, 0, 0, 1.0, 0.0});
-    cv.push_back({J.Vs, J.n, J.Vout, J.ldv, J.n, rk[j], 0, 1.0});
+    J.out_rank = J.s ? rk[j] : 0;
+    h->max_sweeps = std::max(h->max_sweeps, J.s ? sw[j] : 0);
+    // one-sided Jacobi: per sweep s(s-1)/2 pairs x (3 dots + rotation) = 12 n flops each
+    if (g_prof.on && J.s) g_prof.add_work(K_JACOBI, 6.0 * J.n * (double)J.s * (J.s - 1) * sw[j], 0);
+    const int k = J.out_rank;
+    if (k > h->cap) throw CudaError(cudaErrorMemoryAllocation, "tile rank exceeds max_rank capacity", __FILE__, __LINE__);
+    if (!k) continue;
+    cv.push_back({J.Vs, J.n, J.Vout, J.ldv, J.n, k, 0, 1.0, 0, d_perm + (size_t)j * h->nb});
+    gu.push_back({J.E, J.Vout, nullptr, J.Uout, J.m, k, J.n, J.m, J.ldv, J.ldu, J.ldu, 0, 0, 0, 1.0, 0.0});
   }
-  launch_gemm(gu, h->ar, s);
   launch_copy(cv, h->ar, s);
+  launch_gemm(gu, h->ar, s);
 }
 
 int sketch_guess(int prev_rank, int n) {
@@ -549,6 +530,7 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
   TLRB_CUDA(cudaSetDevice(h->device));
   cudaStream_t s = h->stream;
   const auto t0 = std::chrono::steady_clock::now();
+  TLRB_CUDA(cudaEventRecord(h->ev[5], s));
   TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double),
                             z_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   rc = factorize(h, th1, th2, th3, nugget, acc);
@@ -572,6 +554,7 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
     TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[2], h->ev[3])); S.ms_factor = a;
     TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[3], h->ev[4])); S.ms_solve = a;
     S.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[5], h->ev[4])); S.ms_device = a;
     int64_t reals = 0;
     int mx = 0;
     double sum = 0;
@@ -672,11 +655,12 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     h->ws_bytes = std::max((size_t)h->max_jobs * h->slot_doubles * 8, nb2 * 8 * 4);
     TLRB_CUDA(cudaMalloc(&h->ws, h->ws_bytes));
     TLRB_CUDA(cudaMalloc(&h->d_sums, 6 * (size_t)h->max_jobs * sizeof(double)));
-    TLRB_CUDA(cudaMalloc(&h->d_aux, 2 * (size_t)h->max_jobs * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_aux, 3 * (size_t)h->max_jobs * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_kind, (size_t)h->max_jobs * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_ok, (size_t)h->max_jobs * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_rank, (size_t)h->max_jobs * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_sweeps, (size_t)h->max_jobs * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_perm, (size_t)h->max_jobs * h->nb * sizeof(int)));
     return TLRB_OK;
   });
   if (rc != TLRB_OK) {
@@ -693,7 +677,7 @@ void tlrb_destroy(tlrb_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   void* ptrs[] = {h->dx, h->dy, h->diag, h->U, h->V, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
-                  h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_ux, h->d_uy,
+                  h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_ux, h->d_uy,
                   h->d_pred, h->d_partial};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -874,5 +858,26 @@ int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc, in
 }
 
 int64_t tlrb_launch_count(void) { return g_launches; }
+
+int32_t tlrb_profile_enable(int32_t on) {
+  g_prof.reset();
+  g_prof.on = on != 0;
+  return TLRB_OK;
+}
+
+int32_t tlrb_profile_read(int32_t cls, char* name, int32_t len, double* ms, double* flops, double* bytes,
+                          int64_t* launches) {
+  if (cls < 0 || cls >= K_NCLASS) return TLRB_ERR_ARG;
+  g_prof.drain();
+  if (name && len > 0) {
+    strncpy(name, kclass_name[cls], len - 1);
+    name[len - 1] = 0;
+  }
+  if (ms) *ms = g_prof.ms[cls];
+  if (flops) *flops = g_prof.flops[cls];
+  if (bytes) *bytes = g_prof.bytes[cls];
+  if (launches) *launches = g_prof.count[cls];
+  return TLRB_OK;
+}
 
 }  // extern "C"

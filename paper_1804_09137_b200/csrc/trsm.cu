@@ -132,6 +132,12 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
   const TrsmProb* dp = ar.put(keep, s);
   const int* ds = ar.put(start, s);
   const int threads = 32 * W;
+  double fl = 0, by = 0;
+  for (const TrsmProb& p : keep) {
+    fl += (double)p.n * p.n * p.nrhs;
+    by += 8.0 * ((double)p.n * p.n / 2 + 2.0 * p.n * p.nrhs);
+  }
+  ProfScope ps(K_TRSM, s, fl, by);
   if (trans) {
     TLRB_CUDA(cudaFuncSetAttribute(trsm_vbatch_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -215,6 +221,9 @@ __global__ void __launch_bounds__(512) potrf_block_kernel(double* A, int ld, int
 
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s) {
+  const double rest = n - r0 - bs;
+  ProfScope ps(K_POTRF, s, (double)bs * bs * bs / 3 + rest * bs * bs,
+               8.0 * (bs * bs * 2.0 + 2.0 * rest * bs));
   potrf_block_kernel<<<1, 512, 0, s>>>(A, ld, n, r0, bs, tile, info, logdiag);
   post_launch();
 }
