@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include <cfloat>
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -36,31 +37,8 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// rotate columns a and b (length m, shared memory); true if rotated
-__device__ __forceinline__ bool rotate_pair(double* a, double* b, int m, double tol, double tiny2,
-                                            int lane) {
-  double al = 0.0, be = 0.0, ga = 0.0;
-  for (int r = lane; r < m; r += 32) {
-    const double x = a[r], y = b[r];
-    al = fma(x, x, al);
-    be = fma(y, y, be);
-    ga = fma(x, y, ga);
-  }
-  al = wsum(al);
-  be = wsum(be);
-  ga = wsum(ga);
-  if (ga == 0.0 || al <= tiny2 || be <= tiny2) return false;
-  if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) return false;
-  const double zeta = (be - al) / (2.0 * ga);
-  const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-  const double c = 1.0 / sqrt(1.0 + t * t);
-  const double sn = c * t;
-  for (int r = lane; r < m; r += 32) {
-    const double x = a[r], y = b[r];
-    a[r] = c * x - sn * y;
-    b[r] = sn * x + c * y;
-  }
-  return true;
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // round-robin tournament over nplayers (even): match idx of round r
@@ -75,6 +53,36 @@ __device__ __forceinline__ void match(int r, int idx, int np, int& p, int& q) {
   }
 }
 
+// Cross rotation of a register-resident column xa (rows lane + 32 i) with a
+// register copy xb; returns true if rotated (al, be updated).
+template <int RPL>
+__device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL], double& al, double& be,
+                                            double tol, double tiny2) {
+  if (al <= tiny2 || be <= tiny2) return false;
+  double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPL; i += 2) {
+    g0 = fma(xa[i], xb[i], g0);
+    if (i + 1 < RPL) g1 = fma(xa[i + 1], xb[i + 1], g1);
+  }
+  const double ga = wsum(g0 + g1);
+  if (ga == 0.0 || ga * ga <= (tol * tol) * (al * be)) return false;
+  const double zeta = (be - al) / (2.0 * ga);
+  const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+  const double c = rsqrt(fma(t, t, 1.0));
+  const double sn = c * t;
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const double x = xa[i], y = xb[i];
+    xa[i] = fma(c, x, -sn * y);
+    xb[i] = fma(sn, x, c * y);
+  }
+  al = fma(-t, ga, al);
+  be = fma(t, ga, be);
+  return true;
+}
+
+template <int RPL>
 __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
                                                              int max_sweeps) {
   extern __shared__ double sm[];
@@ -87,6 +95,8 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* _
   const int nthr = blockDim.x;
   double* S0 = sm;
   double* S1 = sm + (size_t)B * m;
+  __shared__ double nrm[2][16];      // maintained squared column norms of S0 / S1
+  __shared__ volatile int ver[16];   // rotations completed on each S1 column (this visit)
   __shared__ int rot_flag;
   // rotation tolerance: LAPACK dgesvj's m*eps, tightened for very small acc
   // (the truncated product M V V^T inherits the columns' non-orthogonality);
@@ -99,28 +109,68 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* _
   const int np = nblk + (nblk & 1);   // pad with a dummy block
   int sweeps = 0;
 
+  // load a block into shared memory (flat, many loads in flight)
   auto load = [&](double* dst, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     for (int e = threadIdx.x; e < m * B; e += nthr) {
-      const int r = e % m, c = e / m;
+      const int c = e / m, r = e - c * m;
       dst[c * m + r] = (c < nc) ? __ldcg(P.X + (size_t)(c0 + c) * P.ldx + r) : 0.0;
+    }
+  };
+  auto norms_of = [&](const double* src, double* nr) {
+    for (int c = warp; c < B; c += nw) {
+      double a0 = 0.0, a1 = 0.0;
+      int r = lane;
+      for (; r + 32 < m; r += 64) {
+        a0 = fma(src[c * m + r], src[c * m + r], a0);
+        a1 = fma(src[c * m + r + 32], src[c * m + r + 32], a1);
+      }
+      if (r < m) a0 = fma(src[c * m + r], src[c * m + r], a0);
+      const double a = wsum(a0 + a1);
+      if (lane == 0) nr[c] = a;
     }
   };
   auto store = [&](const double* src, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     for (int e = threadIdx.x; e < m * nc; e += nthr) {
-      const int r = e % m, c = e / m;
+      const int c = e / m, r = e - c * m;
       __stcg(P.X + (size_t)(c0 + c) * P.ldx + r, src[c * m + r]);
     }
   };
-  auto within = [&](double* S, int nc, bool& any) {   // all pairs inside one block
+  auto ld_col = [&](double (&x)[RPL], const double* col) {
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      x[i] = r < m ? col[r] : 0.0;
+    }
+  };
+  auto st_col = [&](const double (&x)[RPL], double* col) {
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      if (r < m) col[r] = x[i];
+    }
+  };
+  // all pairs inside one block: round-robin tournament among B/2 warps
+  // (warps [base, base + B/2)), synchronised on their own named barrier
+  auto within = [&](double* S, double* nr, int nc, int base, int bar_id, bool& any) {
+    const int w = warp - base;
     for (int r = 0; r < B - 1; ++r) {
-      if (warp < B / 2) {
-        int p, q;
-        match(r, warp, B, p, q);
-        if (p < nc && q < nc) any |= rotate_pair(S + p * m, S + q * m, m, tol, tiny2, lane);
+      int p, q;
+      match(r, w, B, p, q);
+      if (p < nc && q < nc) {
+        double xa[RPL], xb[RPL];
+        ld_col(xa, S + p * m);
+        ld_col(xb, S + q * m);
+        double al = nr[p], be = nr[q];
+        if (rotate_regs<RPL>(xa, xb, al, be, tol, tiny2)) {
+          any = true;
+          st_col(xa, S + p * m);
+          st_col(xb, S + q * m);
+          if (lane == 0) { nr[p] = al; nr[q] = be; }
+        }
       }
-      __syncthreads();
+      named_bar(bar_id, B * 16);
     }
   };
 
@@ -135,22 +185,51 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* _
           const bool realJ = J < nblk;
           load(S0, I);
           if (realJ) load(S1, J);
+          if (threadIdx.x < 16) ver[threadIdx.x] = 0;
+          __syncthreads();
+          norms_of(S0, nrm[0]);
+          if (realJ) norms_of(S1, nrm[1]);
           __syncthreads();
           const int ncI = min(B, s - I * B);
           const int ncJ = realJ ? min(B, s - J * B) : 0;
-          if (r == 0) {
-            within(S0, ncI, any);
-            if (realJ) within(S1, ncJ, any);
+          if (r == 0) {   // pairs inside blocks I and J, concurrently on two warp halves
+            if (warp < B / 2) within(S0, nrm[0], ncI, 0, 1, any);
+            else if (realJ && warp < B) within(S1, nrm[1], ncJ, B / 2, 2, any);
+            __syncthreads();
           }
-          if (realJ) {
+          if (realJ && warp < B) {
+            // warp w keeps column w of block I in registers and meets the J
+            // columns in order w, w+1, ...; it only waits for the warp that
+            // used its next J column in the previous round
+            const int p = warp;
+            double xa[RPL], xb[RPL];
+            ld_col(xa, S0 + p * m);
+            double al = nrm[0][p];
+            bool dirty = false;
             for (int rr = 0; rr < B; ++rr) {
-              if (warp < B) {
-                const int p = warp, q = (warp + rr) % B;
-                if (p < ncI && q < ncJ) any |= rotate_pair(S0 + p * m, S1 + q * m, m, tol, tiny2, lane);
+              const int q = (p + rr) % B;
+              if (lane == 0)
+                while (ver[q] != rr) {
+                }
+              __syncwarp();
+              __threadfence_block();
+              if (p < ncI && q < ncJ) {
+                ld_col(xb, S1 + q * m);
+                double be = nrm[1][q];
+                if (rotate_regs<RPL>(xa, xb, al, be, tol, tiny2)) {
+                  any = true;
+                  dirty = true;
+                  st_col(xb, S1 + q * m);
+                  if (lane == 0) nrm[1][q] = be;
+                }
               }
-              __syncthreads();
+              __threadfence_block();
+              __syncwarp();
+              if (lane == 0) ver[q] = rr + 1;
             }
+            if (dirty) st_col(xa, S0 + p * m);
           }
+          __syncthreads();
           store(S0, I);
           if (realJ) store(S1, J);
           __syncthreads();
@@ -237,40 +316,87 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
   int B = 16;
   while (B > 2 && (size_t)2 * B * mmax * 8 > 200 * 1024) B >>= 1;
   // group by cluster size: one CTA per block pair of a round, at most 8
-  std::vector<JacobiProb> groups[4];
+  static int max_g = [] {
+    const char* e = getenv("TLRB_JACOBI_MAXCL");
+    const int v = e ? atoi(e) : 16;
+    return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0;
+  }();
+  std::vector<JacobiProb> groups[5];
   for (const JacobiProb& p : probs) {
     const int nblk = (p.s + B - 1) / B;
     const int pairs = (nblk + 1) / 2;
-    const int g = pairs <= 1 ? 0 : pairs <= 2 ? 1 : pairs <= 4 ? 2 : 3;
+    int g = pairs <= 1 ? 0 : pairs <= 2 ? 1 : pairs <= 4 ? 2 : pairs <= 8 ? 3 : 4;
+    g = std::min(g, max_g);
     groups[g].push_back(p);
   }
-  for (int g = 0; g < 4; ++g) {
+  // independent problem groups run concurrently: the largest-cluster group
+  // on the caller's stream, the others on side streams forked/joined with
+  // events (they would otherwise serialise behind each other)
+  static cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  static cudaEvent_t fork_ev = nullptr, join_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (!fork_ev) {
+    TLRB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    for (int i = 0; i < 4; ++i) {
+      TLRB_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+      TLRB_CUDA(cudaEventCreateWithFlags(&join_ev[i], cudaEventDisableTiming));
+    }
+  }
+  const JacobiProb* dps[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int ngroups = 0;
+  for (int g = 0; g < 5; ++g)
+    if (!groups[g].empty()) { dps[g] = ar.put(groups[g], s); ++ngroups; }
+  if (ngroups > 1) TLRB_CUDA(cudaEventRecord(fork_ev, s));
+  int used_side = 0;
+  bool joined[4] = {false, false, false, false};
+  for (int g = 4; g >= 0; --g) {
     if (groups[g].empty()) continue;
+    cudaStream_t st = s;
+    int side_idx = -1;
+    if (ngroups > 1 && used_side < 4) {
+      // the largest non-empty group stays on s
+      bool larger_exists = false;
+      for (int h = g + 1; h < 5; ++h) larger_exists |= !groups[h].empty();
+      if (larger_exists) {
+        side_idx = used_side++;
+        st = side[side_idx];
+        TLRB_CUDA(cudaStreamWaitEvent(st, fork_ev, 0));
+      }
+    }
     const int CL = 1 << g;
     int smax = 1;
     for (const JacobiProb& p : groups[g]) smax = std::max(smax, p.s);
     const size_t smem = std::max((size_t)2 * B * mmax * 8, (size_t)smax * 12 + 64);
-    TLRB_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    const JacobiProb* dp = ar.put(groups[g], s);
+    auto kern = mmax <= 512 ? jacobi_cluster_kernel<16>
+              : mmax <= 768 ? jacobi_cluster_kernel<24>
+              : mmax <= 1024 ? jacobi_cluster_kernel<32> : jacobi_cluster_kernel<64>;
+    TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     double by = 0;
     for (const JacobiProb& p : groups[g]) by += 8.0 * 3.0 * p.m * p.s;
-    ProfScope ps(K_JACOBI, s, 0, by);  // flops added once the sweep counts are known
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(groups[g].size() * CL));
-    cfg.blockDim = dim3(32 * B);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    TLRB_CUDA(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, dp, B, 60));
-    post_launch();
+    {
+      ProfScope ps(K_JACOBI, st, 0, by);  // flops added once the sweep counts are known
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(groups[g].size() * CL));
+      cfg.blockDim = dim3(32 * B);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, dps[g], B, 60));
+      post_launch();
+    }
+    if (side_idx >= 0) {
+      TLRB_CUDA(cudaEventRecord(join_ev[side_idx], st));
+      joined[side_idx] = true;
+    }
   }
+  for (int i = 0; i < 4; ++i)
+    if (joined[i]) TLRB_CUDA(cudaStreamWaitEvent(s, join_ev[i], 0));
 }
 
 }  // namespace tlrb

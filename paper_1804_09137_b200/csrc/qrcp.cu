@@ -23,6 +23,7 @@ __device__ __forceinline__ double wsum_q(double v) {
   return v;
 }
 
+template <int RPL>
 __global__ void __launch_bounds__(1024) qrcp_kernel(const QrcpProb* __restrict__ probs) {
   extern __shared__ double sm[];
   const QrcpProb P = probs[blockIdx.x];
@@ -148,19 +149,36 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const QrcpProb* __restrict__
     }
     __syncthreads();
     const double tau = s_tau;
-    // apply H_j to trailing columns; recompute partial norms over rows > j
+    // apply H_j to trailing columns; recompute partial norms over rows > j.
+    // Each warp owns whole columns; a column segment A[j:, c] is held in
+    // registers (RPL rows per lane, loads issued back to back).
     for (int c = j + 1 + warp; c < n; c += nw) {
       double* col = A + (size_t)c * lda;
-      double w = 0.0;
-      for (int r = j + lane; r < m; r += 32) w = fma(v[r], col[r], w);
-      w = wsum_q(w) * tau;
-      double a = 0.0;
-      for (int r = j + lane; r < m; r += 32) {
-        const double x = col[r] - w * v[r];
-        col[r] = x;
-        if (r > j) a = fma(x, x, a);
+      double x[RPL];
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = j + lane + 32 * i;
+        x[i] = r < m ? col[r] : 0.0;
       }
-      a = wsum_q(a);
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = j + lane + 32 * i;
+        const double vr = r < m ? v[r] : 0.0;
+        if (i & 1) w1 = fma(vr, x[i], w1); else w0 = fma(vr, x[i], w0);
+      }
+      const double w = wsum_q(w0 + w1) * tau;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = j + lane + 32 * i;
+        if (r < m) {
+          const double y = x[i] - w * v[r];
+          col[r] = y;
+          if (r > j) { if (i & 1) a1 = fma(y, y, a1); else a0 = fma(y, y, a0); }
+        }
+      }
+      const double a = wsum_q(a0 + a1);
       if (lane == 0) cn[c] = a;
     }
     __syncthreads();
@@ -190,10 +208,11 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t
     by += 16.0 * p.m * p.n;
   }
   const size_t smem = (size_t)(nmax + mmax + 64) * 8 + (size_t)(nmax + 32) * 4;
-  TLRB_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = mmax <= 512 ? qrcp_kernel<16> : mmax <= 1024 ? qrcp_kernel<32> : qrcp_kernel<64>;
+  TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const QrcpProb* dp = ar.put(probs, s);
   ProfScope ps(K_QR, s, fl, by);
-  qrcp_kernel<<<(unsigned)probs.size(), 1024, smem, s>>>(dp);
+  kern<<<(unsigned)probs.size(), 1024, smem, s>>>(dp);
   post_launch();
 }
 
