@@ -117,8 +117,9 @@ struct JacobiProb {        // one-sided Jacobi on the columns of X (m x s)
 struct SumsqProb { const double* A; int ld, m, n; double* out; };
 // dst(r, c) = scale * (transpose ? src(c, r) : src(r, c)); tri: zero where r < c;
 // rowperm: dst row rowperm[r] receives row r
+// srccol (transpose mode): dst row r reads source column srccol[r]
 struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale;
-                  int tri; const int* rowperm; };
+                  int tri; const int* rowperm; const int* srccol = nullptr; };
 struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid_out; double stop_rel2; };
 struct GaussProb { double* A; int ld, m, n; uint64_t seed; };
 
@@ -147,7 +148,7 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
 void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
-void launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s);
+bool launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);

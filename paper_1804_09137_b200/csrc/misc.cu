@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyProb* __restrict__ 
   const int64_t e0 = part * per, e1 = min(tot, e0 + per);
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const int r = (int)(e % P.m), c = (int)(e / P.m);
-    double v = P.transpose ? P.src[(size_t)r * P.lds + c] : P.src[(size_t)c * P.lds + r];
+    double v = P.transpose ? P.src[(size_t)(P.srccol ? P.srccol[r] : r) * P.lds + c]
+                           : P.src[(size_t)c * P.lds + r];
     if (P.tri && r < c) v = 0.0;
     const int rd = P.rowperm ? P.rowperm[r] : r;
     P.dst[(size_t)c * P.ldd + rd] = P.scale * v;

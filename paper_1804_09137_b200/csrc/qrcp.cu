@@ -14,8 +14,14 @@
 // and every step streams the trailing columns once (warp per column:
 // load, dot with the reflector, update, recompute the partial norm, store).
 #include "common.cuh"
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+namespace cg = cooperative_groups;
 
 namespace tlrb {
+
+__device__ __forceinline__ double A_ld(const double* a, size_t i) { return __ldcg(a + i); }
 
 __device__ __forceinline__ double wsum_q(double v) {
 #pragma unroll
@@ -196,8 +202,197 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const QrcpProb* __restrict__
   for (int c = tid; c < n; c += blockDim.x) P.perm[c] = perm[c];
 }
 
-void launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s) {
-  if (probs.empty()) return;
+
+// ---------------------------------------------------------------------------
+// Cluster variant: the n columns are split into slabs of cpc columns, one slab
+// per CTA of a (<=16) thread-block cluster, held in shared memory for the
+// whole factorisation.  Columns are never moved: step j picks the pivot by a
+// cluster-wide argmax through distributed shared memory, the owner CTA forms
+// the reflector in place and every CTA reads it through DSMEM and updates its
+// own slab.  perm[0..r) = pivot order, perm[r..n) = the remaining columns in
+// index order.  Two cluster barriers per step; no global-memory traffic
+// besides the initial load and the final write-back.
+template <int RPL>
+__global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __restrict__ probs, int cpc) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const QrcpProb P = probs[blockIdx.x / CL];
+  const int m = P.m, n = P.n, lda = P.lda;
+  const int c_lo = crank * cpc, c_hi = min(n, c_lo + cpc), nloc = max(0, c_hi - c_lo);
+  double* Ac = sm;                          // cpc x m (column c_lo + k at Ac + k*m)
+  double* vb = Ac + (size_t)cpc * m;        // 2 x m reflector buffers (by step parity)
+  double* cn = vb + 2 * (size_t)m;          // cpc partial norms^2
+  __shared__ double pub_val[2], pub_sum[2], pub_tau[2];
+  __shared__ int pub_idx[2], pub_cnt;
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_piv, s_stop;
+  __shared__ double s_tau, s_total, s_resid;
+  __shared__ unsigned char done[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int kmax = min(m, n);
+
+  for (int e = tid; e < nloc * m; e += blockDim.x) {
+    const int k = e / m, r = e - k * m;
+    Ac[(size_t)k * m + r] = A_ld(P.A, (size_t)(c_lo + k) * lda + r);
+  }
+  if (tid < 64) done[tid] = 0;
+  __syncthreads();
+  for (int k = warp; k < nloc; k += nw) {
+    double a = 0.0;
+    for (int r = lane; r < m; r += 32) a = fma(Ac[(size_t)k * m + r], Ac[(size_t)k * m + r], a);
+    a = wsum_q(a);
+    if (lane == 0) cn[k] = a;
+  }
+  __syncthreads();
+  // total ||M||^2 = sum over the cluster (fixed order -> identical everywhere)
+  if (tid == 0) {
+    double a = 0.0;
+    for (int k = 0; k < nloc; ++k) a += cn[k];
+    pub_sum[1] = a;
+  }
+  cl.sync();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int c = 0; c < CL; ++c) t += *cl.map_shared_rank(&pub_sum[1], c);
+    s_total = t;
+  }
+  __syncthreads();
+  const double total = s_total;
+  if (crank == 0 && tid == 0) P.resid_out[-1] = total;
+  const double stop = P.stop_rel2 * total;
+  int j = 0;
+  double resid = total;
+  for (; j < kmax; ++j) {
+    const int par = j & 1;
+    // local candidate: argmax of remaining partial norms + their sum
+    if (warp == 0) {
+      double best = -1.0, sum = 0.0;
+      int bi = n;
+      for (int k = lane; k < nloc; k += 32)
+        if (!done[k]) {
+          sum += cn[k];
+          if (cn[k] > best) { best = cn[k]; bi = c_lo + k; }
+        }
+      sum = wsum_q(sum);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) { pub_val[par] = best; pub_idx[par] = bi; pub_sum[par] = sum; }
+    }
+    cl.sync();
+    if (tid == 0) {
+      double best = -1.0, t = 0.0;
+      int bi = n;
+      for (int c = 0; c < CL; ++c) {
+        const double ov = *cl.map_shared_rank(&pub_val[par], c);
+        const int oi = *cl.map_shared_rank(&pub_idx[par], c);
+        t += *cl.map_shared_rank(&pub_sum[par], c);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      s_piv = bi;
+      s_resid = t;
+      s_stop = (t <= stop) ? 1 : 0;
+    }
+    __syncthreads();
+    resid = s_resid;
+    if (s_stop) break;
+    const int p = s_piv;
+    const int owner = p / cpc;
+    if (crank == owner && warp == 0) {   // reflector of column p, rows j..m-1
+      double* col = Ac + (size_t)(p - c_lo) * m;
+      double ss = 0.0;
+      for (int r = j + 1 + lane; r < m; r += 32) ss = fma(col[r], col[r], ss);
+      ss = wsum_q(ss);
+      const double alpha = col[j];
+      double tau = 0.0, beta = alpha, scale = 1.0;
+      if (ss != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      double* v = vb + (size_t)par * m;
+      for (int r = j + 1 + lane; r < m; r += 32) {
+        const double x = col[r] * scale;
+        col[r] = x;
+        v[r] = x;
+      }
+      if (lane == 0) {
+        v[j] = 1.0;
+        col[j] = beta;
+        pub_tau[par] = tau;
+        done[p - c_lo] = 1;
+        P.perm[j] = p;
+      }
+    }
+    cl.sync();
+    // fetch the reflector from the owner's shared memory
+    const double* rv = cl.map_shared_rank(vb + (size_t)par * m, owner);
+    double* v = vb + (size_t)par * m;
+    if (crank != owner)
+      for (int r = j + tid; r < m; r += blockDim.x) v[r] = rv[r];
+    if (tid == 0) s_tau = *cl.map_shared_rank(&pub_tau[par], owner);
+    __syncthreads();
+    const double tau = s_tau;
+    for (int k = warp; k < nloc; k += nw) {
+      if (done[k]) continue;
+      double* col = Ac + (size_t)k * m;
+      double x[RPL];
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = j + lane + 32 * i;
+        x[i] = r < m ? col[r] : 0.0;
+        const double vr = r < m ? v[r] : 0.0;
+        if (i & 1) w1 = fma(vr, x[i], w1); else w0 = fma(vr, x[i], w0);
+      }
+      const double w = wsum_q(w0 + w1) * tau;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = j + lane + 32 * i;
+        if (r < m) {
+          const double y = x[i] - w * v[r];
+          col[r] = y;
+          if (r > j) { if (i & 1) a1 = fma(y, y, a1); else a0 = fma(y, y, a0); }
+        }
+      }
+      const double a = wsum_q(a0 + a1);
+      if (lane == 0) cn[k] = a;
+    }
+    __syncthreads();
+  }
+  // write the slab back; remaining columns go to perm[j..n) in index order
+  for (int e = tid; e < nloc * m; e += blockDim.x) {
+    const int k = e / m, r = e - k * m;
+    P.A[(size_t)(c_lo + k) * lda + r] = Ac[(size_t)k * m + r];
+  }
+  if (tid == 0) {
+    int cnt = 0;
+    for (int k = 0; k < nloc; ++k) cnt += !done[k];
+    pub_cnt = cnt;
+  }
+  cl.sync();
+  if (tid == 0) {
+    int off = j;
+    for (int c = 0; c < crank; ++c) off += *cl.map_shared_rank(&pub_cnt, c);
+    for (int k = 0; k < nloc; ++k)
+      if (!done[k]) P.perm[off++] = c_lo + k;
+    if (crank == 0) {
+      *P.r_out = j;
+      *P.resid_out = (j < kmax) ? resid : 0.0;
+    }
+  }
+  cl.sync();   // keep shared memory alive until every remote read is done
+}
+
+bool launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return false;
   int mmax = 1, nmax = 1;
   double fl = 0, by = 0;
   for (const QrcpProb& p : probs) {
@@ -207,6 +402,36 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t
     fl += 4.0 * p.m * p.n * k - 2.0 * (p.m + p.n) * k * k + 4.0 / 3.0 * k * k * k;
     by += 16.0 * p.m * p.n;
   }
+  // cluster path: column slabs in shared memory of up to 16 CTAs
+  const size_t budget = 200 * 1024;
+  int cpc = (int)((budget - 2 * (size_t)mmax * 8) / ((size_t)mmax * 8 + 8));
+  cpc = std::min(cpc, 64);
+  const int CL = (nmax + cpc - 1) / cpc;
+  static const bool no_cluster = getenv("TLRB_QRCP_NOCLUSTER") != nullptr;
+  if (!no_cluster && cpc >= 8 && CL <= 16 && mmax <= 1024) {
+    cpc = (nmax + CL - 1) / CL;
+    const size_t smem = ((size_t)cpc * mmax + 2 * (size_t)mmax + cpc) * 8;
+    auto kern = mmax <= 512 ? qrcp_cluster_kernel<16> : qrcp_cluster_kernel<32>;
+    TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const QrcpProb* dp = ar.put(probs, s);
+    ProfScope ps(K_QR, s, fl, by);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(probs.size() * CL));
+    cfg.blockDim = dim3(mmax <= 512 ? 1024 : 512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, dp, cpc));
+    post_launch();
+    return true;   // columns stay in place: R column jj lives at perm[jj]
+  }
   const size_t smem = (size_t)(nmax + mmax + 64) * 8 + (size_t)(nmax + 32) * 4;
   auto kern = mmax <= 512 ? qrcp_kernel<16> : mmax <= 1024 ? qrcp_kernel<32> : qrcp_kernel<64>;
   TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -214,6 +439,7 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t
   ProfScope ps(K_QR, s, fl, by);
   kern<<<(unsigned)probs.size(), 1024, smem, s>>>(dp);
   post_launch();
+  return false;    // columns physically pivoted: R column jj lives at jj
 }
 
 }  // namespace tlrb

@@ -102,6 +102,14 @@ struct tlrb_handle {
 
 namespace {
 
+bool trace_on() {
+  static const bool on = getenv("TLRB_TRACE") != nullptr;
+  return on;
+}
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 // ------------------------------------------------------------ compression
 struct Job {
   int m, n;           // M is m x n
@@ -141,6 +149,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   if (!nj) return;
   cudaStream_t s = h->stream;
   int* d_perm = reinterpret_cast<int*>(h->d_perm);
+  bool gathered = false;
   {
     std::vector<CopyProb> cp;
     std::vector<QrcpProb> qp;
@@ -151,11 +160,13 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
                     (kSketchRelTol * acc) * (kSketchRelTol * acc)});
     }
     launch_copy(cp, h->ar, s);
-    launch_qrcp(qp, h->ar, s);
+    gathered = launch_qrcp(qp, h->ar, s);
   }
   std::vector<int> rr(nj);
   TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  const double t_q0 = trace_on() ? now_ms() : 0;
   h->sync();
+  const double t_q1 = trace_on() ? now_ms() : 0;
   std::vector<int> kinds(nj);
   {
     std::vector<CopyProb> cp;
@@ -164,7 +175,9 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
       J.s = rr[j];
       kinds[j] = 1 | (J.kind & 2);   // e2 = QRCP residual (sums[6j+1])
       // X (n x r): X(p, c) = R(c, p) for p >= c
-      if (J.s) cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.s, 1, 1.0, 1, nullptr});
+      if (J.s)
+        cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.s, 1, 1.0, 1, nullptr,
+                      gathered ? d_perm + (size_t)j * h->nb : nullptr});
     }
     launch_copy(cp, h->ar, s);
   }
@@ -183,6 +196,12 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   TLRB_CUDA(cudaMemcpyAsync(rk.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
   TLRB_CUDA(cudaMemcpyAsync(sw.data(), h->d_sweeps, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
   h->sync();
+  if (trace_on()) {
+    int rmax = 0, smax = 0;
+    for (int j = 0; j < nj; ++j) { rmax = std::max(rmax, rr[j]); smax = std::max(smax, sw[j]); }
+    fprintf(stderr, "[tlrb] compress nj=%d  prep+qrcp %.2f ms (wait %.2f)  jacobi %.2f ms  rmax=%d sweeps<=%d\n", nj,
+            t_q1 - t_q0, t_q1 - t_q0, now_ms() - t_q1, rmax, smax);
+  }
   std::vector<GemmProb> gu;
   std::vector<CopyProb> cv;
   for (int j = 0; j < nj; ++j) {
@@ -332,6 +351,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
   const int t = h->t, nb = h->nb;
   double* tmp = reinterpret_cast<double*>(h->ws);  // small products before the job batch
   for (int k = 0; k < t; ++k) {
+    const double tk0 = trace_on() ? now_ms() : 0;
     potrf(h, k);
     // K4: V_ik <- L_kk^-1 V_ik
     std::vector<TrsmProb> tp;
@@ -372,6 +392,10 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_gemm(g1, h->ar, h->stream);
       launch_gemm(g2, h->ar, h->stream);
       launch_gemm(g3, h->ar, h->stream);
+    }
+    if (trace_on()) {
+      h->sync();
+      fprintf(stderr, "[tlrb] step %d potrf+trsm+syrk %.2f ms\n", k, now_ms() - tk0);
     }
     // K6 + K7: updates of (i, j), i > j > k, in job batches
     std::vector<std::pair<int, int>> upd;
