@@ -120,7 +120,8 @@ struct SumsqProb { const double* A; int ld, m, n; double* out; };
 // srccol (transpose mode): dst row r reads source column srccol[r]
 struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale;
                   int tri; const int* rowperm; const int* srccol = nullptr; };
-struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid_out; double stop_rel2; };
+struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid_out; double stop_rel2;
+                  int hint = 0; };   // hint: predicted number of QRCP steps (selects the kernel)
 struct GaussProb { double* A; int ld, m, n; uint64_t seed; };
 
 // Device-resident descriptor staging (pinned host ring -> device), reset at
@@ -148,7 +149,9 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
 void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
-bool launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s);
+// gathered[p] = 1: columns left in place (R column jj at perm[jj]); 0: physically pivoted
+void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered, DescArena& ar,
+                 cudaStream_t s);
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);

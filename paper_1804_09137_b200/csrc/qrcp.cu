@@ -391,55 +391,105 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
   cl.sync();   // keep shared memory alive until every remote read is done
 }
 
-bool launch_qrcp(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s) {
-  if (probs.empty()) return false;
-  int mmax = 1, nmax = 1;
+struct QrcpLaunch {
+  const QrcpProb* dp = nullptr;
+  int count = 0, mmax = 1, nmax = 1;
   double fl = 0, by = 0;
+};
+
+static QrcpLaunch stage(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s) {
+  QrcpLaunch L;
+  L.count = (int)probs.size();
   for (const QrcpProb& p : probs) {
-    mmax = std::max(mmax, p.m);
-    nmax = std::max(nmax, p.n);
-    const double k = std::min(p.m, p.n);
-    fl += 4.0 * p.m * p.n * k - 2.0 * (p.m + p.n) * k * k + 4.0 / 3.0 * k * k * k;
-    by += 16.0 * p.m * p.n;
+    L.mmax = std::max(L.mmax, p.m);
+    L.nmax = std::max(L.nmax, p.n);
+    const double k = std::min(p.m, std::max(1, p.hint));
+    L.fl += 4.0 * p.m * p.n * k - 2.0 * (p.m + p.n) * k * k + 4.0 / 3.0 * k * k * k;
+    L.by += 16.0 * p.m * p.n;
   }
-  // cluster path: column slabs in shared memory of up to 16 CTAs
+  if (L.count) L.dp = ar.put(probs, s);
+  return L;
+}
+
+static int cluster_cpc(int mmax, int nmax, int& CL) {
   const size_t budget = 200 * 1024;
   int cpc = (int)((budget - 2 * (size_t)mmax * 8) / ((size_t)mmax * 8 + 8));
   cpc = std::min(cpc, 64);
-  const int CL = (nmax + cpc - 1) / cpc;
-  static const bool no_cluster = getenv("TLRB_QRCP_NOCLUSTER") != nullptr;
-  if (!no_cluster && cpc >= 8 && CL <= 16 && mmax <= 1024) {
-    cpc = (nmax + CL - 1) / CL;
-    const size_t smem = ((size_t)cpc * mmax + 2 * (size_t)mmax + cpc) * 8;
-    auto kern = mmax <= 512 ? qrcp_cluster_kernel<16> : qrcp_cluster_kernel<32>;
-    TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    const QrcpProb* dp = ar.put(probs, s);
-    ProfScope ps(K_QR, s, fl, by);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(probs.size() * CL));
-    cfg.blockDim = dim3(mmax <= 512 ? 1024 : 512);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, dp, cpc));
-    post_launch();
-    return true;   // columns stay in place: R column jj lives at perm[jj]
-  }
-  const size_t smem = (size_t)(nmax + mmax + 64) * 8 + (size_t)(nmax + 32) * 4;
-  auto kern = mmax <= 512 ? qrcp_kernel<16> : mmax <= 1024 ? qrcp_kernel<32> : qrcp_kernel<64>;
+  CL = (nmax + cpc - 1) / cpc;
+  if (cpc < 8 || CL > 16 || mmax > 1024) return 0;
+  return (nmax + CL - 1) / CL;
+}
+
+static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
+  int CL = 0;
+  const int cpc = cluster_cpc(L.mmax, L.nmax, CL);
+  const size_t smem = ((size_t)cpc * L.mmax + 2 * (size_t)L.mmax + cpc) * 8;
+  auto kern = L.mmax <= 512 ? qrcp_cluster_kernel<16> : qrcp_cluster_kernel<32>;
   TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const QrcpProb* dp = ar.put(probs, s);
-  ProfScope ps(K_QR, s, fl, by);
-  kern<<<(unsigned)probs.size(), 1024, smem, s>>>(dp);
+  if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  ProfScope ps(K_QR, s, L.fl, L.by);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(L.count * CL));
+  cfg.blockDim = dim3(L.mmax <= 512 ? 1024 : 512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, L.dp, cpc));
   post_launch();
-  return false;    // columns physically pivoted: R column jj lives at jj
+}
+
+static void run_single(const QrcpLaunch& L, cudaStream_t s) {
+  const size_t smem = (size_t)(L.nmax + L.mmax + 64) * 8 + (size_t)(L.nmax + 32) * 4;
+  auto kern = L.mmax <= 512 ? qrcp_kernel<16> : L.mmax <= 1024 ? qrcp_kernel<32> : qrcp_kernel<64>;
+  TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfScope ps(K_QR, s, L.fl, L.by);
+  kern<<<(unsigned)L.count, 1024, smem, s>>>(L.dp);
+  post_launch();
+}
+
+// Problems with a large predicted rank go to the cluster kernel (latency:
+// ~3 us per pivot step on 16 SMs); the rest to the one-CTA kernel (throughput:
+// they finish in few steps).  The two groups run concurrently (side stream
+// forked after the descriptors are staged, joined before returning).
+void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered, DescArena& ar,
+                 cudaStream_t s) {
+  gathered.assign(probs.size(), 0);
+  if (probs.empty()) return;
+  static const bool no_cluster = getenv("TLRB_QRCP_NOCLUSTER") != nullptr;
+  static const int thr = getenv("TLRB_QRCP_CLUSTER_MIN") ? atoi(getenv("TLRB_QRCP_CLUSTER_MIN")) : 160;
+  std::vector<QrcpProb> big, small;
+  std::vector<int> big_idx;
+  int mmax = 1, nmax = 1;
+  for (const QrcpProb& p : probs) { mmax = std::max(mmax, p.m); nmax = std::max(nmax, p.n); }
+  int CL = 0;
+  const bool cluster_ok = !no_cluster && cluster_cpc(mmax, nmax, CL) > 0;
+  for (size_t i = 0; i < probs.size(); ++i) {
+    if (cluster_ok && probs[i].hint > thr) { big.push_back(probs[i]); big_idx.push_back((int)i); }
+    else small.push_back(probs[i]);
+  }
+  const QrcpLaunch Lb = stage(big, ar, s), Ls = stage(small, ar, s);
+  if (!Lb.count) { run_single(Ls, s); return; }
+  for (int i : big_idx) gathered[i] = 1;
+  if (!Ls.count) { run_cluster(Lb, s); return; }
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  if (!side) {
+    TLRB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    TLRB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    TLRB_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+  }
+  TLRB_CUDA(cudaEventRecord(fork_ev, s));
+  TLRB_CUDA(cudaStreamWaitEvent(side, fork_ev, 0));
+  run_single(Ls, side);
+  run_cluster(Lb, s);
+  TLRB_CUDA(cudaEventRecord(join_ev, side));
+  TLRB_CUDA(cudaStreamWaitEvent(s, join_ev, 0));
 }
 
 }  // namespace tlrb

@@ -149,7 +149,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   if (!nj) return;
   cudaStream_t s = h->stream;
   int* d_perm = reinterpret_cast<int*>(h->d_perm);
-  bool gathered = false;
+  std::vector<char> gathered;
   {
     std::vector<CopyProb> cp;
     std::vector<QrcpProb> qp;
@@ -157,10 +157,10 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
       Job& J = jobs[j];
       cp.push_back({J.M, J.m, J.E, J.m, J.m, J.n, 0, 1.0, 0, nullptr});
       qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, h->d_rank + j, h->d_sums + 6 * j + 1,
-                    (kSketchRelTol * acc) * (kSketchRelTol * acc)});
+                    (kSketchRelTol * acc) * (kSketchRelTol * acc), J.s});
     }
     launch_copy(cp, h->ar, s);
-    gathered = launch_qrcp(qp, h->ar, s);
+    launch_qrcp(qp, gathered, h->ar, s);
   }
   std::vector<int> rr(nj);
   TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -177,7 +177,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
       // X (n x r): X(p, c) = R(c, p) for p >= c
       if (J.s)
         cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.s, 1, 1.0, 1, nullptr,
-                      gathered ? d_perm + (size_t)j * h->nb : nullptr});
+                      gathered[j] ? d_perm + (size_t)j * h->nb : nullptr});
     }
     launch_copy(cp, h->ar, s);
   }
@@ -260,7 +260,7 @@ void compress_all(tlrb_handle* h, double acc) {
       J.n = h->sz[j];
       // initial sketch: ranks grow towards the diagonal
       const int off = i - j;
-      J.s = off <= 2 ? J.n : std::min(J.n, 64);
+      J.s = off <= 2 ? J.n : std::min(J.n, 64);   // QRCP kernel hint (predicted steps)
       J.kind = 0;
       J.Uout = h->Ut(i, j);
       J.Vout = h->Vt(i, j);
