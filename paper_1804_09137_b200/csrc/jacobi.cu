@@ -110,13 +110,36 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* _
   const int np = nblk + (nblk & 1);   // pad with a dummy block
   int sweeps = 0;
 
-  // load a block into shared memory (flat, many loads in flight)
+  // load a block into shared memory: 16-byte cp.async (LDGSTS) when the
+  // columns are 16-byte aligned, so every load of the block is in flight at
+  // once; completed by cp_wait() before the next barrier
+  const bool vec = ((m & 1) == 0) && ((P.ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.X) & 15) == 0);
   auto load = [&](double* dst, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
-    for (int e = threadIdx.x; e < m * B; e += nthr) {
-      const int c = e / m, r = e - c * m;
-      dst[c * m + r] = (c < nc) ? __ldcg(P.X + (size_t)(c0 + c) * P.ldx + r) : 0.0;
+    if (vec) {
+      const int mh = m >> 1;
+      for (int e = threadIdx.x; e < mh * B; e += nthr) {
+        const int c = e / mh, r = 2 * (e - c * mh);
+        double* d = dst + c * m + r;
+        if (c < nc) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                       "l"(P.X + (size_t)(c0 + c) * P.ldx + r));
+        } else {
+          d[0] = 0.0;
+          d[1] = 0.0;
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    } else {
+      for (int e = threadIdx.x; e < m * B; e += nthr) {
+        const int c = e / m, r = e - c * m;
+        dst[c * m + r] = (c < nc) ? __ldcg(P.X + (size_t)(c0 + c) * P.ldx + r) : 0.0;
+      }
     }
+  };
+  auto cp_wait = [&]() {
+    if (vec) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   };
   auto norms_of = [&](const double* src, double* nr) {
     for (int c = warp; c < B; c += nw) {
@@ -186,6 +209,7 @@ __global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* _
           const bool realJ = J < nblk;
           load(S0, I);
           if (realJ) load(S1, J);
+          cp_wait();
           __syncthreads();
           norms_of(S0, nrm[0]);
           if (realJ) norms_of(S1, nrm[1]);
@@ -359,7 +383,11 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     const int CL = 1 << g;
     int smax = 1;
     for (const JacobiProb& p : groups[g]) smax = std::max(smax, p.s);
-    const size_t smem = std::max((size_t)2 * B * mmax * 8, (size_t)smax * 12 + 64);
+    // block width so that a round has (close to) one block pair per CTA:
+    // nblk = 2 CL blocks of width ceil(smax / 2CL), even, <= B
+    int Bg = (smax + 2 * CL - 1) / (2 * CL);
+    Bg = std::min(B, std::max(2, (Bg + 1) & ~1));
+    const size_t smem = std::max((size_t)2 * Bg * mmax * 8, (size_t)smax * 12 + 64);
     auto kern = mmax <= 512 ? jacobi_cluster_kernel<16>
               : mmax <= 768 ? jacobi_cluster_kernel<24>
               : mmax <= 1024 ? jacobi_cluster_kernel<32> : jacobi_cluster_kernel<64>;
@@ -371,7 +399,7 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
       ProfScope ps(K_JACOBI, st, 0, by);  // flops added once the sweep counts are known
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(groups[g].size() * CL));
-      cfg.blockDim = dim3(32 * B);
+      cfg.blockDim = dim3(32 * Bg);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
@@ -381,7 +409,7 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, dps[g], B, 60));
+      TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, dps[g], Bg, 60));
       post_launch();
     }
     if (side_idx >= 0) {

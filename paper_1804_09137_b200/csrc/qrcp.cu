@@ -254,10 +254,10 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
     pub_sum[1] = a;
   }
   cl.sync();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int c = 0; c < CL; ++c) t += *cl.map_shared_rank(&pub_sum[1], c);
-    s_total = t;
+  if (warp == 0) {
+    double t = lane < CL ? *cl.map_shared_rank(&pub_sum[1], lane) : 0.0;
+    t = wsum_q(t);
+    if (lane == 0) s_total = t;
   }
   __syncthreads();
   const double total = s_total;
@@ -286,18 +286,26 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
       if (lane == 0) { pub_val[par] = best; pub_idx[par] = bi; pub_sum[par] = sum; }
     }
     cl.sync();
-    if (tid == 0) {
+    if (warp == 0) {   // lane c reads CTA c's candidate (remote loads in parallel)
       double best = -1.0, t = 0.0;
       int bi = n;
-      for (int c = 0; c < CL; ++c) {
-        const double ov = *cl.map_shared_rank(&pub_val[par], c);
-        const int oi = *cl.map_shared_rank(&pub_idx[par], c);
-        t += *cl.map_shared_rank(&pub_sum[par], c);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      if (lane < CL) {
+        best = *cl.map_shared_rank(&pub_val[par], lane);
+        bi = *cl.map_shared_rank(&pub_idx[par], lane);
+        t = *cl.map_shared_rank(&pub_sum[par], lane);
       }
-      s_piv = bi;
-      s_resid = t;
-      s_stop = (t <= stop) ? 1 : 0;
+      t = wsum_q(t);   // fixed shuffle tree: identical in every CTA
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        s_piv = bi;
+        s_resid = t;
+        s_stop = (t <= stop) ? 1 : 0;
+      }
     }
     __syncthreads();
     resid = s_resid;

@@ -857,7 +857,7 @@ int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc, in
     bind_slot(h, J, 0);
     J.m = m;
     J.n = n;
-    J.s = std::min(n, 64);
+    J.s = n;   // QRCP kernel hint: unknown rank, assume large
     J.kind = 0;
     J.Uout = h->diag;  // the diag arena (nb x nb) receives U (m x k)
     double* dv;
