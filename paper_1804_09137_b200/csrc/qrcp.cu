@@ -206,12 +206,15 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const QrcpProb* __restrict__
 // ---------------------------------------------------------------------------
 // Cluster variant: the n columns are split into slabs of cpc columns, one slab
 // per CTA of a (<=16) thread-block cluster, held in shared memory for the
-// whole factorisation.  Columns are never moved: step j picks the pivot by a
-// cluster-wide argmax through distributed shared memory, the owner CTA forms
-// the reflector in place and every CTA reads it through DSMEM and updates its
-// own slab.  perm[0..r) = pivot order, perm[r..n) = the remaining columns in
-// index order.  Two cluster barriers per step; no global-memory traffic
-// besides the initial load and the final write-back.
+// whole factorisation.  Columns are never moved.  One cluster barrier per
+// pivot step: after it, every CTA reads all published candidates (argmax of
+// remaining partial norms + their sums) through distributed shared memory,
+// fetches the pivot column from its owner (DSMEM) and forms the Householder
+// reflector itself — the same data and the same reduction order give the
+// same reflector in every CTA — then updates its own slab and publishes its
+// candidate for the next step.  The owner writes the reflector into the
+// pivot column only after the next barrier (others may still be reading it).
+// perm[0..r) = pivot order, perm[r..n) = the remaining columns in index order.
 template <int RPL>
 __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __restrict__ probs, int cpc) {
   extern __shared__ double sm[];
@@ -222,14 +225,13 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
   const int m = P.m, n = P.n, lda = P.lda;
   const int c_lo = crank * cpc, c_hi = min(n, c_lo + cpc), nloc = max(0, c_hi - c_lo);
   double* Ac = sm;                          // cpc x m (column c_lo + k at Ac + k*m)
-  double* vb = Ac + (size_t)cpc * m;        // 2 x m reflector buffers (by step parity)
-  double* cn = vb + 2 * (size_t)m;          // cpc partial norms^2
-  __shared__ double pub_val[2], pub_sum[2], pub_tau[2];
+  double* v = Ac + (size_t)cpc * m;         // m: reflector of the current step
+  double* cn = v + m;                       // cpc partial norms^2
+  __shared__ double pub_val[2], pub_sum[2];
   __shared__ int pub_idx[2], pub_cnt;
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
+  __shared__ double red[32];
   __shared__ int s_piv, s_stop;
-  __shared__ double s_tau, s_total, s_resid;
+  __shared__ double s_resid, s_total, s_beta, s_tau, s_scale;
   __shared__ unsigned char done[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int kmax = min(m, n);
@@ -247,27 +249,8 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
     if (lane == 0) cn[k] = a;
   }
   __syncthreads();
-  // total ||M||^2 = sum over the cluster (fixed order -> identical everywhere)
-  if (tid == 0) {
-    double a = 0.0;
-    for (int k = 0; k < nloc; ++k) a += cn[k];
-    pub_sum[1] = a;
-  }
-  cl.sync();
-  if (warp == 0) {
-    double t = lane < CL ? *cl.map_shared_rank(&pub_sum[1], lane) : 0.0;
-    t = wsum_q(t);
-    if (lane == 0) s_total = t;
-  }
-  __syncthreads();
-  const double total = s_total;
-  if (crank == 0 && tid == 0) P.resid_out[-1] = total;
-  const double stop = P.stop_rel2 * total;
-  int j = 0;
-  double resid = total;
-  for (; j < kmax; ++j) {
-    const int par = j & 1;
-    // local candidate: argmax of remaining partial norms + their sum
+  // local candidate for step `step` into pub[par]
+  auto publish = [&](int par) {
     if (warp == 0) {
       double best = -1.0, sum = 0.0;
       int bi = n;
@@ -285,8 +268,35 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
       }
       if (lane == 0) { pub_val[par] = best; pub_idx[par] = bi; pub_sum[par] = sum; }
     }
-    cl.sync();
-    if (warp == 0) {   // lane c reads CTA c's candidate (remote loads in parallel)
+  };
+  publish(0);
+  cl.sync();
+  // ||M||^2 = sum of the step-0 sums (fixed shuffle tree: identical everywhere)
+  if (warp == 0) {
+    double t = lane < CL ? *cl.map_shared_rank(&pub_sum[0], lane) : 0.0;
+    t = wsum_q(t);
+    if (lane == 0) s_total = t;
+  }
+  __syncthreads();
+  const double total = s_total;
+  if (crank == 0 && tid == 0) P.resid_out[-1] = total;
+  const double stop = P.stop_rel2 * total;
+  int j = 0, pend = -1;   // pend: local index of the owned pivot column awaiting its reflector write
+  double pend_beta = 0.0;
+  int pend_j = 0;
+  double resid = total;
+  auto flush_pending = [&]() {
+    if (pend >= 0) {
+      double* col = Ac + (size_t)pend * m;
+      for (int r = pend_j + 1 + tid; r < m; r += blockDim.x) col[r] = v[r];
+      if (tid == 0) col[pend_j] = pend_beta;
+      __syncthreads();
+      pend = -1;
+    }
+  };
+  for (; j < kmax; ++j) {
+    const int par = j & 1;
+    if (warp == 0) {
       double best = -1.0, t = 0.0;
       int bi = n;
       if (lane < CL) {
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
         bi = *cl.map_shared_rank(&pub_idx[par], lane);
         t = *cl.map_shared_rank(&pub_sum[par], lane);
       }
-      t = wsum_q(t);   // fixed shuffle tree: identical in every CTA
+      t = wsum_q(t);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -308,45 +318,52 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
       }
     }
     __syncthreads();
+    // the previous step's pivot column may be written now (everyone is past
+    // the barrier, so nobody reads it any more); v is still that reflector
+    flush_pending();
     resid = s_resid;
     if (s_stop) break;
     const int p = s_piv;
     const int owner = p / cpc;
-    if (crank == owner && warp == 0) {   // reflector of column p, rows j..m-1
-      double* col = Ac + (size_t)(p - c_lo) * m;
-      double ss = 0.0;
-      for (int r = j + 1 + lane; r < m; r += 32) ss = fma(col[r], col[r], ss);
+    if (crank == 0 && tid == 0) P.perm[j] = p;
+    // fetch the pivot column (rows j..m-1) from its owner
+    const double* src = cl.map_shared_rank(sm, owner) + (size_t)(p - owner * cpc) * m;
+    double part = 0.0;
+    for (int r = j + tid; r < m; r += blockDim.x) {
+      const double x = src[r];
+      v[r] = x;
+      if (r > j) part = fma(x, x, part);
+    }
+    part = wsum_q(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (warp == 0) {
+      double ss = lane < nw ? red[lane] : 0.0;
       ss = wsum_q(ss);
-      const double alpha = col[j];
-      double tau = 0.0, beta = alpha, scale = 1.0;
-      if (ss != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      double* v = vb + (size_t)par * m;
-      for (int r = j + 1 + lane; r < m; r += 32) {
-        const double x = col[r] * scale;
-        col[r] = x;
-        v[r] = x;
-      }
       if (lane == 0) {
-        v[j] = 1.0;
-        col[j] = beta;
-        pub_tau[par] = tau;
-        done[p - c_lo] = 1;
-        P.perm[j] = p;
+        const double alpha = v[j];
+        double tau = 0.0, beta = alpha, scale = 1.0;
+        if (ss != 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+          tau = (beta - alpha) / beta;
+          scale = 1.0 / (alpha - beta);
+        }
+        s_beta = beta;
+        s_tau = tau;
+        s_scale = scale;
       }
     }
-    cl.sync();
-    // fetch the reflector from the owner's shared memory
-    const double* rv = cl.map_shared_rank(vb + (size_t)par * m, owner);
-    double* v = vb + (size_t)par * m;
-    if (crank != owner)
-      for (int r = j + tid; r < m; r += blockDim.x) v[r] = rv[r];
-    if (tid == 0) s_tau = *cl.map_shared_rank(&pub_tau[par], owner);
     __syncthreads();
-    const double tau = s_tau;
+    const double tau = s_tau, scale = s_scale;
+    for (int r = j + 1 + tid; r < m; r += blockDim.x) v[r] *= scale;
+    if (tid == 0) v[j] = 1.0;
+    if (crank == owner) {
+      pend = p - c_lo;
+      pend_beta = s_beta;
+      pend_j = j;
+      if (tid == 0) done[pend] = 1;
+    }
+    __syncthreads();
     for (int k = warp; k < nloc; k += nw) {
       if (done[k]) continue;
       double* col = Ac + (size_t)k * m;
@@ -374,7 +391,10 @@ __global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __re
       if (lane == 0) cn[k] = a;
     }
     __syncthreads();
+    publish(par ^ 1);
+    cl.sync();
   }
+  flush_pending();
   // write the slab back; remaining columns go to perm[j..n) in index order
   for (int e = tid; e < nloc * m; e += blockDim.x) {
     const int k = e / m, r = e - k * m;
@@ -431,7 +451,7 @@ static int cluster_cpc(int mmax, int nmax, int& CL) {
 static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
   int CL = 0;
   const int cpc = cluster_cpc(L.mmax, L.nmax, CL);
-  const size_t smem = ((size_t)cpc * L.mmax + 2 * (size_t)L.mmax + cpc) * 8;
+  const size_t smem = ((size_t)cpc * L.mmax + (size_t)L.mmax + cpc) * 8;
   auto kern = L.mmax <= 512 ? qrcp_cluster_kernel<16> : qrcp_cluster_kernel<32>;
   TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

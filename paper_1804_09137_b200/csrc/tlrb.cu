@@ -163,8 +163,9 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     launch_qrcp(qp, gathered, h->ar, s);
   }
   std::vector<int> rr(nj);
-  TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
   const double t_q0 = trace_on() ? now_ms() : 0;
+  if (trace_on()) h->sync();
+  TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
   h->sync();
   const double t_q1 = trace_on() ? now_ms() : 0;
   std::vector<int> kinds(nj);
@@ -199,8 +200,8 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   if (trace_on()) {
     int rmax = 0, smax = 0;
     for (int j = 0; j < nj; ++j) { rmax = std::max(rmax, rr[j]); smax = std::max(smax, sw[j]); }
-    fprintf(stderr, "[tlrb] compress nj=%d  prep+qrcp %.2f ms (wait %.2f)  jacobi %.2f ms  rmax=%d sweeps<=%d\n", nj,
-            t_q1 - t_q0, t_q1 - t_q0, now_ms() - t_q1, rmax, smax);
+    fprintf(stderr, "[tlrb] compress nj=%d  qrcp %.2f ms  jacobi %.2f ms  rmax=%d sweeps<=%d\n", nj,
+            t_q1 - t_q0, now_ms() - t_q1, rmax, smax);
   }
   std::vector<GemmProb> gu;
   std::vector<CopyProb> cv;
