@@ -84,8 +84,8 @@ __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL]
   return true;
 }
 
-template <int RPL>
-__global__ void __launch_bounds__(512) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
+template <int RPL, int NT>
+__global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
                                                              int max_sweeps) {
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -388,9 +388,12 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     int Bg = (smax + 2 * CL - 1) / (2 * CL);
     Bg = std::min(B, std::max(2, (Bg + 1) & ~1));
     const size_t smem = std::max((size_t)2 * Bg * mmax * 8, (size_t)smax * 12 + 64);
-    auto kern = mmax <= 512 ? jacobi_cluster_kernel<16>
-              : mmax <= 768 ? jacobi_cluster_kernel<24>
-              : mmax <= 1024 ? jacobi_cluster_kernel<32> : jacobi_cluster_kernel<64>;
+    // rows per lane and the thread bound (registers: 2 RPL doubles per lane)
+    auto kern = mmax <= 512 ? jacobi_cluster_kernel<16, 512>
+              : mmax <= 768 ? jacobi_cluster_kernel<24, 512>
+              : mmax <= 1024 ? jacobi_cluster_kernel<32, 256> : jacobi_cluster_kernel<64, 128>;
+    const int bmax = mmax <= 768 ? 16 : mmax <= 1024 ? 8 : 4;
+    if (Bg > bmax) Bg = bmax;
     TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     double by = 0;

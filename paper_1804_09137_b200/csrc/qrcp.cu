@@ -29,8 +29,8 @@ __device__ __forceinline__ double wsum_q(double v) {
   return v;
 }
 
-template <int RPL>
-__global__ void __launch_bounds__(1024) qrcp_kernel(const QrcpProb* __restrict__ probs) {
+template <int RPL, int NT>
+__global__ void __launch_bounds__(NT) qrcp_kernel(const QrcpProb* __restrict__ probs) {
   extern __shared__ double sm[];
   const QrcpProb P = probs[blockIdx.x];
   const int m = P.m, n = P.n, lda = P.lda;
@@ -215,8 +215,8 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const QrcpProb* __restrict__
 // candidate for the next step.  The owner writes the reflector into the
 // pivot column only after the next barrier (others may still be reading it).
 // perm[0..r) = pivot order, perm[r..n) = the remaining columns in index order.
-template <int RPL>
-__global__ void __launch_bounds__(1024) qrcp_cluster_kernel(const QrcpProb* __restrict__ probs, int cpc) {
+template <int RPL, int NT>
+__global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __restrict__ probs, int cpc) {
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks();
@@ -452,13 +452,13 @@ static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
   int CL = 0;
   const int cpc = cluster_cpc(L.mmax, L.nmax, CL);
   const size_t smem = ((size_t)cpc * L.mmax + (size_t)L.mmax + cpc) * 8;
-  auto kern = L.mmax <= 512 ? qrcp_cluster_kernel<16> : qrcp_cluster_kernel<32>;
+  auto kern = L.mmax <= 512 ? qrcp_cluster_kernel<16, 1024> : qrcp_cluster_kernel<32, 512>;
   TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   ProfScope ps(K_QR, s, L.fl, L.by);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(L.count * CL));
-  cfg.blockDim = dim3(L.mmax <= 512 ? 1024 : 512);
+  cfg.blockDim = dim3(L.mmax <= 512 ? 1024 : 512);   // = NT of the instantiation
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -474,10 +474,12 @@ static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
 
 static void run_single(const QrcpLaunch& L, cudaStream_t s) {
   const size_t smem = (size_t)(L.nmax + L.mmax + 64) * 8 + (size_t)(L.nmax + 32) * 4;
-  auto kern = L.mmax <= 512 ? qrcp_kernel<16> : L.mmax <= 1024 ? qrcp_kernel<32> : qrcp_kernel<64>;
+  auto kern = L.mmax <= 512 ? qrcp_kernel<16, 1024> : L.mmax <= 1024 ? qrcp_kernel<32, 512>
+                                                     : qrcp_kernel<64, 256>;
+  const int nt = L.mmax <= 512 ? 1024 : L.mmax <= 1024 ? 512 : 256;
   TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfScope ps(K_QR, s, L.fl, L.by);
-  kern<<<(unsigned)L.count, 1024, smem, s>>>(L.dp);
+  kern<<<(unsigned)L.count, nt, smem, s>>>(L.dp);
   post_launch();
 }
 

@@ -188,3 +188,36 @@ def test_deterministic(tb):
     z = np.random.default_rng(5).standard_normal(300)
     cfg = tb.LikelihoodConfig(mode="tlr", accuracy=1e-7, nb=64)
     assert tb.log_likelihood(locs, z, p, cfg) == tb.log_likelihood(locs, z, p, cfg)
+
+
+def _patch(tb, name):
+    import json
+    p = GOLD / "patches.json"
+    if not p.exists():
+        pytest.skip("patch goldens not generated")
+    d = json.loads(p.read_text())
+    if name not in d:
+        pytest.skip(f"{name} golden missing")
+    e = d[name]
+    full = tb.generate_locations(e["parent_n"], 0).coords
+    sel = (full[:, 0] < e["edge"]) & (full[:, 1] < e["edge"])
+    locs = tb.LocationSet(full[sel])
+    assert len(locs) == e["n"]
+    z = np.load(GOLD / "z_patches.npz")[name]
+    return e, locs, z
+
+
+@pytest.mark.parametrize("name", ["C3p", "C4p", "C5p"])
+def test_patch_parity(tb, name):
+    """Geometry-matched 10K patches of C3/C4/C5: same point
+    density, theta, nb and acc as the full configs; the reference runs them."""
+    e, locs, z = _patch(tb, name)
+    p = tb.MaternParams(*e["theta"])
+    for mode, r in e["modes"].items():
+        acc = None if mode == "dense" else float(mode.split(":")[1])
+        cfg = tb.LikelihoodConfig(nb=e["nb"]) if acc is None else \
+            tb.LikelihoodConfig(mode="tlr", accuracy=acc, nb=e["nb"])
+        ll, ld, q, st = tb.log_likelihood_parts(locs, z, p, cfg)
+        tol = 1e-10 if acc is None else max(1e-8, 10 * acc)
+        rel = abs(ll - r["ll"]) / abs(r["ll"])
+        assert rel <= tol, (name, mode, ll, r["ll"], rel)
