@@ -80,6 +80,10 @@ void* DescArena::put_bytes(const void* src, size_t bytes, cudaStream_t s) {
 // ------------------------------------------------------------ sum of squares
 __global__ void __launch_bounds__(256) sumsq_kernel(const SumsqProb* __restrict__ probs) {
   const SumsqProb P = probs[blockIdx.x];
+  if (P.A == nullptr) {   // constant entry: *out = m (used as ||V||^2 = rank of an orthonormal V)
+    if (threadIdx.x == 0) *P.out = (double)P.m;
+    return;
+  }
   double a = 0.0;
   const int64_t tot = (int64_t)P.m * P.n;
   for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {

@@ -58,6 +58,7 @@ struct tlrb_handle {
   double* V = nullptr;
   size_t slab = 0;               // doubles per U (or V) slab
   std::vector<int> rank;         // per lower tile
+  std::vector<char> dense;       // per lower tile: stored dense (rank > max_rank), as L_ij^T in the U slab
   int* d_info = nullptr;         // [flag, tile, pivot]
   double* d_logdiag = nullptr;   // n
   double* d_scal = nullptr;      // [logdet, quad]
@@ -90,6 +91,8 @@ struct tlrb_handle {
   int retries = 0, max_sweeps = 0;
 
   size_t tid(int i, int j) const { return (size_t)i * (i - 1) / 2 + j; }
+  bool dn(int i, int j) const { return dense[tid(i, j)] != 0; }
+  bool live(int i, int j) const { return dense[tid(i, j)] || rank[tid(i, j)] > 0; }
   double* Ut(int i, int j) const { return U + tid(i, j) * slab; }
   double* Vt(int i, int j) const { return V + tid(i, j) * slab; }
   double* D(int i) const { return diag + (size_t)i * nb * nb; }
@@ -119,6 +122,7 @@ struct Job {
   double* E; double* Y; double* Q; double* Om; double* Bt; double* Vs; double* sig; double* T;
   double* Uout; double* Vout; int ldu, ldv;
   int out_rank;
+  bool dense_out;     // rank above max_rank: stored dense (L^T in Uout, ld ldu)
   uint64_t seed;
 };
 
@@ -212,7 +216,12 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     // one-sided Jacobi: per sweep s(s-1)/2 pairs x (3 dots + rotation) = 12 n flops each
     if (g_prof.on && J.s) g_prof.add_work(K_JACOBI, 6.0 * J.n * (double)J.s * (J.s - 1) * sw[j], 0);
     const int k = J.out_rank;
-    if (k > h->cap) throw CudaError(cudaErrorMemoryAllocation, "tile rank exceeds max_rank capacity", __FILE__, __LINE__);
+    J.dense_out = h->max_rank > 0 && k > h->max_rank;
+    if (J.dense_out) {   // A13: over the storage cap -> keep the tile exact (dense, transposed)
+      cv.push_back({J.E, J.m, J.Uout, J.ldu, J.n, J.m, 1, 1.0, 0, nullptr});
+      continue;
+    }
+    if (k > h->cap) throw CudaError(cudaErrorMemoryAllocation, "tile rank exceeds slab capacity", __FILE__, __LINE__);
     if (!k) continue;
     cv.push_back({J.Vs, J.n, J.Vout, J.ldv, J.n, k, 0, 1.0, 0, d_perm + (size_t)j * h->nb});
     gu.push_back({J.E, J.Vout, nullptr, J.Uout, J.m, k, J.n, J.m, J.ldv, J.ldu, J.ldu, 0, 0, 0, 1.0, 0.0});
@@ -274,7 +283,8 @@ void compress_all(tlrb_handle* h, double acc) {
     compress_jobs(h, jobs, acc);
     for (size_t q = c0; q < c1; ++q) {
       const Job& J = jobs[q - c0];
-      h->rank[h->tid(all[q].first, all[q].second)] = J.out_rank;
+      h->rank[h->tid(all[q].first, all[q].second)] = J.dense_out ? 0 : J.out_rank;
+      h->dense[h->tid(all[q].first, all[q].second)] = J.dense_out;
       const double m = J.m, n = J.n, k = J.out_rank;
       h->work.add(4.0 * m * n * k, 8.0 * m * n + 8.0 * k * (m + n));
     }
@@ -354,22 +364,34 @@ bool factor_tlr(tlrb_handle* h, double acc) {
   for (int k = 0; k < t; ++k) {
     const double tk0 = trace_on() ? now_ms() : 0;
     potrf(h, k);
-    // K4: V_ik <- L_kk^-1 V_ik
+    // K4: V_ik <- L_kk^-1 V_ik (low-rank) / L_ik^T <- L_kk^-1 A_ik^T (dense, A13)
     std::vector<TrsmProb> tp;
     for (int i = k + 1; i < t; ++i) {
+      const double nk = h->sz[k];
+      if (h->dn(i, k)) {
+        tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
+        h->work.add(nk * nk * h->sz[i], 8.0 * (nk * nk / 2 + 2.0 * nk * h->sz[i]));
+        continue;
+      }
       const int r = h->rank[h->tid(i, k)];
       if (r) tp.push_back({h->D(k), nb, h->Vt(i, k), nb, h->sz[k], r});
-      const double nk = h->sz[k];
       if (r) h->work.add(nk * nk * r, 8.0 * (nk * nk / 2 + 2.0 * nk * r));
     }
     launch_trsm(tp, false, h->ar, h->stream);
     if (check_npd(h)) return false;
-    // K5: D_j -= U_jk (V_jk^T V_jk) U_jk^T
+    // K5: D_j -= U_jk (V_jk^T V_jk) U_jk^T  (dense panel tile: D_j -= T_jk^T T_jk)
     {
       std::vector<GemmProb> g1, g2, g3;
       size_t o = 0;
       const size_t ws_doubles = h->ws_bytes / sizeof(double);
       for (int j = k + 1; j < t; ++j) {
+        const double nj = h->sz[j];
+        if (h->dn(j, k)) {
+          g3.push_back({h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
+                        nb, 1, 0, 1, -1.0, 1.0});
+          h->work.add(nj * nj * h->sz[k], 8.0 * (2.0 * nj * h->sz[k] + 2.0 * nj * nj));
+          continue;
+        }
         const int r = h->rank[h->tid(j, k)];
         if (!r) continue;
         if (o + (size_t)r * r + (size_t)h->sz[j] * r > ws_doubles) {
@@ -387,7 +409,6 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         g2.push_back({h->Ut(j, k), X, nullptr, W, h->sz[j], r, r, nb, r, h->sz[j], h->sz[j], 0, 0, 0, 1.0, 0.0});
         g3.push_back({W, h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], r, h->sz[j], nb, nb, nb, 0, 1, 1,
                       -1.0, 1.0});
-        const double nj = h->sz[j];
         h->work.add(4.0 * nj * r * r + 2.0 * nj * nj * r, 8.0 * (2.0 * nj * r + 2.0 * nj * nj));
       }
       launch_gemm(g1, h->ar, h->stream);
@@ -398,20 +419,22 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       h->sync();
       fprintf(stderr, "[tlrb] step %d potrf+trsm+syrk %.2f ms\n", k, now_ms() - tk0);
     }
-    // K6 + K7: updates of (i, j), i > j > k, in job batches
+    // K6 + K7: updates of (i, j), i > j > k, in job batches; a rank-0 panel
+    // tile skips the update exactly like linalg.py:135
     std::vector<std::pair<int, int>> upd;
     for (int j = k + 1; j < t; ++j)
       for (int i = j + 1; i < t; ++i)
-        if (h->rank[h->tid(i, k)] && h->rank[h->tid(j, k)]) upd.push_back({i, j});
+        if (h->live(i, k) && h->live(j, k)) upd.push_back({i, j});
     for (size_t c0 = 0; c0 < upd.size(); c0 += h->max_jobs) {
       const size_t c1 = std::min(upd.size(), c0 + h->max_jobs);
       std::vector<Job> jobs;
       std::vector<GemmProb> gx, gy, gm, gm2;
+      std::vector<CopyProb> cm;
       std::vector<SumsqProb> sq;
-      std::vector<int> kin;
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
         const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], kij = h->rank[h->tid(i, j)];
+        const bool di = h->dn(i, k), dj = h->dn(j, k), dij = h->dn(i, j);
         const int mi = h->sz[i], mj = h->sz[j], mk = h->sz[k];
         Job J{};
         const int slot = (int)(q - c0);
@@ -419,40 +442,70 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         J.m = mi;
         J.n = mj;
         J.kind = 2;
-        J.s = sketch_guess(std::max(kij, kj), mj);
+        J.s = dij ? mj : sketch_guess(std::max(kij, di || dj ? mj : kj), mj);
         J.Uout = h->Ut(i, j);
         J.Vout = h->Vt(i, j);
         J.ldu = J.ldv = nb;
         J.seed = (uint64_t)h->tid(i, j) * 7777 + (uint64_t)k * 131 + 5;
-        double* X = J.E;  // ki x kj
-        double* Y = J.Y;  // mi x kj   (U2 = -Y)
-        gx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, X, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
-        gy.push_back({h->Ut(i, k), X, nullptr, Y, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, 1.0, 0.0});
-        gm.push_back({h->Ut(i, j), h->Vt(i, j), nullptr, J.M, mi, mj, kij, nb, nb, mi, mi, 0, 1, 0, 1.0, 0.0});
-        gm2.push_back({Y, h->Ut(j, k), J.M, J.M, mi, mj, kj, mi, nb, mi, mi, 0, 1, 0, -1.0, 1.0});
+        double* X = J.E;
+        double* Y = J.Y;
         double* S = h->d_sums + 6 * slot;
-        sq.push_back({h->Ut(i, j), nb, mi, kij, S + 2});
-        sq.push_back({Y, mi, mi, kj, S + 3});
-        sq.push_back({h->Vt(i, j), nb, mj, kij, S + 4});
-        sq.push_back({h->Ut(j, k), nb, mj, kj, S + 5});
+        // current tile
+        if (dij) {
+          cm.push_back({h->Ut(i, j), nb, J.M, mi, mi, mj, 1, 1.0, 0, nullptr});
+          sq.push_back({h->Ut(i, j), nb, mj, mi, S + 2});
+          sq.push_back({nullptr, 0, std::min(mi, mj), 0, S + 4});
+        } else {
+          gm.push_back({h->Ut(i, j), h->Vt(i, j), nullptr, J.M, mi, mj, kij, nb, nb, mi, mi, 0, 1, 0, 1.0, 0.0});
+          sq.push_back({h->Ut(i, j), nb, mi, kij, S + 2});
+          sq.push_back({h->Vt(i, j), nb, mj, kij, S + 4});
+        }
+        // M -= L_ik L_jk^T  (compression.py:54-81 operands u2 = -L_ik-part, v2 = L_jk-part)
+        if (!di && !dj) {
+          gx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, X, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
+          gy.push_back({h->Ut(i, k), X, nullptr, Y, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, 1.0, 0.0});
+          gm2.push_back({Y, h->Ut(j, k), J.M, J.M, mi, mj, kj, mi, nb, mi, mi, 0, 1, 0, -1.0, 1.0});
+          sq.push_back({Y, mi, mi, kj, S + 3});
+          sq.push_back({h->Ut(j, k), nb, mj, kj, S + 5});
+        } else if (di && !dj) {
+          gy.push_back({h->Ut(i, k), h->Vt(j, k), nullptr, Y, mi, kj, mk, nb, nb, mi, mi, 1, 0, 0, 1.0, 0.0});
+          gm2.push_back({Y, h->Ut(j, k), J.M, J.M, mi, mj, kj, mi, nb, mi, mi, 0, 1, 0, -1.0, 1.0});
+          sq.push_back({Y, mi, mi, kj, S + 3});
+          sq.push_back({h->Ut(j, k), nb, mj, kj, S + 5});
+        } else if (!di && dj) {
+          gx.push_back({h->Vt(i, k), h->Ut(j, k), nullptr, X, ki, mj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
+          gm2.push_back({h->Ut(i, k), X, J.M, J.M, mi, mj, ki, nb, ki, mi, mi, 0, 0, 0, -1.0, 1.0});
+          sq.push_back({h->Ut(i, k), nb, mi, ki, S + 3});
+          sq.push_back({h->Ut(j, k), nb, mk, mj, S + 5});
+        } else {
+          gm2.push_back({h->Ut(i, k), h->Ut(j, k), J.M, J.M, mi, mj, mk, nb, nb, mi, mi, 1, 0, 0, -1.0, 1.0});
+          sq.push_back({h->Ut(i, k), nb, mk, mi, S + 3});
+          sq.push_back({h->Ut(j, k), nb, mk, mj, S + 5});
+        }
         jobs.push_back(J);
       }
       launch_gemm(gx, h->ar, h->stream);
       launch_gemm(gy, h->ar, h->stream);
       launch_gemm(gm, h->ar, h->stream);
+      launch_copy(cm, h->ar, h->stream);
       launch_gemm(gm2, h->ar, h->stream);
+      // noise-floor norms (Y = U2 exists now; the tile's old factors are
+      // only overwritten at the end of compress_jobs)
       launch_sumsq(sq, h->ar, h->stream);
       compress_jobs(h, jobs, acc);
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
-        const double ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)],
-                     kij = h->rank[h->tid(i, j)];
-        const double kn = jobs[q - c0].out_rank;
+        const double ki = h->dn(i, k) ? h->sz[k] : h->rank[h->tid(i, k)];
+        const double kj = h->dn(j, k) ? h->sz[k] : h->rank[h->tid(j, k)];
+        const double kij = h->dn(i, j) ? h->sz[j] : h->rank[h->tid(i, j)];
+        const Job& J = jobs[q - c0];
+        const double kn = J.dense_out ? h->sz[j] : J.out_rank;
         const double K = kij + kj, Kh = std::min<double>(K, h->nb), nbd = h->sz[i];
         h->work.add(4.0 * nbd * ki * kj + 2.0 * (4.0 * nbd * K * Kh - 4.0 / 3.0 * Kh * Kh * Kh) +
                         24.0 * Kh * Kh * Kh + 4.0 * nbd * Kh * kn,
                     8.0 * nbd * (2 * kij + 2 * ki + 2 * kj + 2 * kn));
-        h->rank[h->tid(i, j)] = jobs[q - c0].out_rank;
+        h->rank[h->tid(i, j)] = J.dense_out ? 0 : J.out_rank;
+        h->dense[h->tid(i, j)] = J.dense_out;
       }
     }
   }
@@ -468,7 +521,7 @@ void forward_solve(tlrb_handle* h) {
     std::vector<GemmProb> g1, g2;
     for (int i = j + 1; i < t; ++i) {
       double* yi = h->d_z + h->off[i];
-      if (h->factor_mode == 1) {  // y_i -= T_ij^T y_j
+      if (h->factor_mode == 1 || h->dn(i, j)) {  // y_i -= T_ij^T y_j
         g1.push_back({h->Ut(i, j), yj, yi, yi, h->sz[i], 1, h->sz[j], nb, h->sz[j], h->sz[i], h->sz[i], 1, 0, 0,
                       -1.0, 1.0});
       } else {
@@ -492,7 +545,7 @@ void backward_solve(tlrb_handle* h) {
     std::vector<GemmProb> g1, g2;
     for (int j = 0; j < i; ++j) {
       double* xj = h->d_z + h->off[j];
-      if (h->factor_mode == 1) {  // x_j -= L_ij^T x_i = T_ij x_i
+      if (h->factor_mode == 1 || h->dn(i, j)) {  // x_j -= L_ij^T x_i = T_ij x_i
         g1.push_back({h->Ut(i, j), xi, xj, xj, h->sz[j], 1, h->sz[i], nb, h->sz[i], h->sz[j], h->sz[j], 0, 0, 0,
                       -1.0, 1.0});
       } else {
@@ -534,6 +587,7 @@ int factorize(tlrb_handle* h, double th1, double th2, double th3, double nugget,
   generate(h, nugget, dense);
   TLRB_CUDA(cudaEventRecord(h->ev[1], s));
   std::fill(h->rank.begin(), h->rank.end(), 0);
+  std::fill(h->dense.begin(), h->dense.end(), 0);
   if (!dense) compress_all(h, acc);
   TLRB_CUDA(cudaEventRecord(h->ev[2], s));
   const bool ok = dense ? factor_dense(h) : factor_tlr(h, acc);
@@ -587,7 +641,7 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
     for (int i = 0; i < h->t; ++i) {
       reals += (int64_t)h->sz[i] * h->sz[i];
       for (int j = 0; j < i; ++j) {
-        if (h->factor_mode == 1) { reals += (int64_t)h->sz[i] * h->sz[j]; continue; }
+        if (h->factor_mode == 1 || h->dn(i, j)) { reals += (int64_t)h->sz[i] * h->sz[j]; continue; }
         const int r = h->rank[h->tid(i, j)];
         reals += (int64_t)r * (h->sz[i] + h->sz[j]);
         mx = std::max(mx, r);
@@ -663,6 +717,7 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMalloc(&h->U, std::max<size_t>(1, ntile * h->slab) * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->V, std::max<size_t>(1, ntile * h->slab) * sizeof(double)));
     h->rank.assign(ntile, 0);
+    h->dense.assign(ntile, 0);
     TLRB_CUDA(cudaMalloc(&h->d_info, 4 * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_logdiag, n * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_scal, 4 * sizeof(double)));
@@ -784,7 +839,7 @@ int32_t tlrb_rank_map(tlrb_handle* h, int32_t* ranks, int32_t cap, int32_t* t_ou
   for (int i = 0; i < h->t * h->t; ++i) ranks[i] = 0;
   for (int i = 1; i < h->t; ++i)
     for (int j = 0; j < i; ++j)
-      ranks[i * h->t + j] = h->factor_mode == 1 ? -1 : h->rank[h->tid(i, j)];
+      ranks[i * h->t + j] = (h->factor_mode == 1 || h->dn(i, j)) ? -1 : h->rank[h->tid(i, j)];
   return TLRB_OK;
 }
 

@@ -221,3 +221,25 @@ def test_patch_parity(tb, name):
         tol = 1e-10 if acc is None else max(1e-8, 10 * acc)
         rel = abs(ll - r["ll"]) / abs(r["ll"])
         assert rel <= tol, (name, mode, ll, r["ll"], rel)
+
+
+@pytest.mark.parametrize("max_rank,accs", [(40, (1e-9, 1e-7)), (120, (1e-9,))])
+def test_max_rank_dense_fallback(tb, gold, max_rank, accs):
+    """A13: tiles whose rank at acc exceeds max_rank are kept dense (exact)
+    instead of truncated further; the result stays within the TLR tolerance
+    of the reference and between the reference TLR and dense values."""
+    e = gold["loglik"]["C1"]
+    locs = tb.generate_locations(e["n"], e["loc_seed"])
+    p = tb.MaternParams(*e["theta"])
+    z = gold["z"]["C1"]
+    for acc in accs:   # uncapped C1 max ranks: 154 (1e-9), 118 (1e-7)
+        cfg = tb.LikelihoodConfig(mode="tlr", accuracy=acc, nb=e["nb"], max_rank=max_rank)
+        ll, _, _, st = tb.log_likelihood_parts(locs, z, p, cfg)
+        ref = e["modes"][f"tlr:{acc:g}"]["ll"]
+        assert abs(ll - ref) <= max(1e-8, 10 * acc) * abs(ref)
+        h = tb.api._handle_for(locs.coords, e["nb"], max_rank, 1)
+        rm = h.rank_map()
+        low = np.tril(rm, -1)
+        assert (low == -1).any()                     # some tiles went dense
+        assert low.max() <= max_rank
+        assert st["max_rank"] <= max_rank
