@@ -75,6 +75,15 @@ int32_t tlrb_loglik_device(tlrb_handle* h, const double* d_z, double theta1,
                            double theta2, double theta3, double nugget, double acc,
                            double* ll, double* logdet, double* quad, tlrb_stats* st);
 
+/* Factorise Sigma(theta) into the handle without a solve (acc == 0: dense).
+ * Used by tlrb_apply_factor / tlrb_solve. */
+int32_t tlrb_factorize(tlrb_handle* h, double theta1, double theta2, double theta3,
+                       double nugget, double acc);
+
+/* y = L x with the current factor (stats.sample_measurements, stats.py:115-133,
+ * draws z = L w with the dense nb = min(200, n) factor).  x, y: host, n. */
+int32_t tlrb_apply_factor(tlrb_handle* h, const double* x, double* y);
+
 /* Solve Sigma x = rhs with the factor of the last successful tlrb_loglik /
  * tlrb_predict call (linalg.solve_cholesky semantics).  rhs, x: host, n. */
 int32_t tlrb_solve(tlrb_handle* h, const double* rhs, double* x);

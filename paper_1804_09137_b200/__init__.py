@@ -16,11 +16,12 @@ from .api import (  # noqa: F401
     log_likelihood_parts,
     matern_block,
     predict,
+    sample_measurements,
 )
 
 __all__ = [
     "DeviceError", "Handle", "LikelihoodConfig", "LocationSet", "MaternParams",
     "NotPositiveDefiniteError", "PredictionProblem", "bessel_k", "compress_tile",
     "generate_locations", "launch_count", "log_likelihood", "log_likelihood_parts",
-    "matern_block", "predict",
+    "matern_block", "predict", "sample_measurements",
 ]

@@ -51,6 +51,9 @@ SIGNATURES = [
                                 C.c_double, _DP, _DP, _DP, C.POINTER(TlrbStats)]),
     ("tlrb_loglik_device", C.c_int32, [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.c_double, _DP, _DP, _DP, C.POINTER(TlrbStats)]),
+    ("tlrb_factorize", C.c_int32, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double,
+                                   C.c_double]),
+    ("tlrb_apply_factor", C.c_int32, [C.c_void_p, _DP, _DP]),
     ("tlrb_solve", C.c_int32, [C.c_void_p, _DP, _DP]),
     ("tlrb_predict", C.c_int32, [C.c_void_p, _DP, _DP, C.c_int64, C.c_double, C.c_double, C.c_double,
                                  C.c_double, C.c_double, _DP]),

@@ -207,6 +207,19 @@ class Handle:
         self.last_stats = st.as_dict()
         return float(out[0]), float(out[1]), float(out[2])
 
+    def factorize(self, p: MaternParams, acc: float | None):
+        rc = self.lib.tlrb_factorize(self.h, p.theta1, p.theta2, p.theta3, p.nugget, float(acc or 0.0))
+        if rc:
+            self._raise(rc)
+
+    def apply_factor(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        rc = self.lib.tlrb_apply_factor(self.h, dptr(x), dptr(y))
+        if rc:
+            self._raise(rc)
+        return y
+
     def solve(self, rhs: np.ndarray) -> np.ndarray:
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
         x = np.empty_like(rhs)
@@ -280,6 +293,21 @@ def log_likelihood_parts(locs, z, p: MaternParams, cfg: LikelihoodConfig = Likel
     h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus)
     ll, ld, q = h.loglik(z, p, cfg.accuracy if cfg.mode == "tlr" else None)
     return ll, ld, q, h.last_stats
+
+
+def sample_measurements(locs, p_true: MaternParams, seed: int) -> np.ndarray:
+    """One zero-mean field realisation z = L w (stats.py:115-133): dense tile
+    Cholesky with nb = min(200, n) on the device, w = default_rng(seed)
+    standard normals (the reference's own stream, drawn on the host)."""
+    coords = _coords_of(locs)
+    n = coords.shape[0]
+    h = Handle(coords, min(DEFAULT_NB_DENSE, n))
+    try:
+        h.factorize(p_true, None)
+        w = np.random.default_rng(seed).standard_normal(n)
+        return h.apply_factor(w)
+    finally:
+        h.close()
 
 
 @dataclass(frozen=True)

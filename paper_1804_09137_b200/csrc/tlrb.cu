@@ -64,6 +64,7 @@ struct tlrb_handle {
   double* d_scal = nullptr;      // [logdet, quad]
   double* d_z = nullptr;         // n (rhs / solution)
   double* d_w = nullptr;         // solve temporaries (t * nb)
+  double* d_y = nullptr;         // y = L x output (n), allocated on first use
   // kriging
   double* d_ux = nullptr; double* d_uy = nullptr; double* d_pred = nullptr;
   double* d_partial = nullptr; int64_t ucap = 0;
@@ -512,6 +513,49 @@ bool factor_tlr(tlrb_handle* h, double acc) {
   return !check_npd(h);
 }
 
+// ------------------------------------------------------------ y = L x
+// (sample_measurements, stats.py:115-133: z = L w tile by tile)
+__global__ void tril_kernel(double* A, int ld, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int r = e % n, c = e / n;
+    if (r < c) A[(size_t)c * ld + r] = 0.0;
+  }
+}
+
+void apply_factor(tlrb_handle* h, const double* dx, double* dy) {
+  const int t = h->t, nb = h->nb;
+  for (int i = 0; i < t; ++i) {   // the diagonal factors' upper parts are stale: clear them
+    tril_kernel<<<64, 256, 0, h->stream>>>(h->D(i), nb, h->sz[i]);
+    post_launch();
+  }
+  // y_i = L_ii x_i, then y_i += L_ij x_j column by column (one launch per j,
+  // every problem of a launch writes a different y_i)
+  std::vector<GemmProb> g0;
+  for (int i = 0; i < t; ++i)
+    g0.push_back({h->D(i), dx + h->off[i], nullptr, dy + h->off[i], h->sz[i], 1, h->sz[i], nb, h->sz[i],
+                  h->sz[i], h->sz[i], 0, 0, 0, 1.0, 0.0});
+  launch_gemm(g0, h->ar, h->stream);
+  for (int j = 0; j < t; ++j) {
+    const double* xj = dx + h->off[j];
+    std::vector<GemmProb> g1, g2;
+    for (int i = j + 1; i < t; ++i) {
+      double* yi = dy + h->off[i];
+      if (h->factor_mode == 1 || h->dn(i, j)) {
+        g1.push_back({h->Ut(i, j), xj, yi, yi, h->sz[i], 1, h->sz[j], nb, h->sz[j], h->sz[i], h->sz[i], 1, 0, 0,
+                      1.0, 1.0});
+      } else {
+        const int r = h->rank[h->tid(i, j)];
+        if (!r) continue;
+        double* w = h->d_w + (size_t)i * nb;
+        g1.push_back({h->Vt(i, j), xj, nullptr, w, r, 1, h->sz[j], nb, h->sz[j], r, r, 1, 0, 0, 1.0, 0.0});
+        g2.push_back({h->Ut(i, j), w, yi, yi, h->sz[i], 1, r, nb, r, h->sz[i], h->sz[i], 0, 0, 0, 1.0, 1.0});
+      }
+    }
+    launch_gemm(g1, h->ar, h->stream);
+    launch_gemm(g2, h->ar, h->stream);
+  }
+}
+
 // ------------------------------------------------------------------ solves
 void forward_solve(tlrb_handle* h) {
   const int t = h->t, nb = h->nb;
@@ -757,7 +801,7 @@ void tlrb_destroy(tlrb_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   void* ptrs[] = {h->dx, h->dy, h->diag, h->U, h->V, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
-                  h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_ux, h->d_uy,
+                  h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_y, h->d_ux, h->d_uy,
                   h->d_pred, h->d_partial};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -779,6 +823,35 @@ int32_t tlrb_loglik_device(tlrb_handle* h, const double* d_z, double th1, double
                            tlrb_stats* st) {
   if (!h || !d_z) return TLRB_ERR_ARG;
   return guarded(h, [&] { return loglik_impl(h, d_z, true, th1, th2, th3, nugget, acc, ll, logdet, quad, st); });
+}
+
+int32_t tlrb_factorize(tlrb_handle* h, double th1, double th2, double th3, double nugget, double acc) {
+  if (!h) return TLRB_ERR_ARG;
+  const int rc = validate(th1, th2, th3, nugget, acc);
+  if (rc) return rc;
+  return guarded(h, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(h->device));
+    const int r = factorize(h, th1, th2, th3, nugget, acc);
+    h->sync();
+    return r;
+  });
+}
+
+int32_t tlrb_apply_factor(tlrb_handle* h, const double* x, double* y) {
+  if (!h || !x || !y) return TLRB_ERR_ARG;
+  if (!h->factor_mode) {
+    h->msg = "no factor available";
+    return TLRB_ERR_ARG;
+  }
+  return guarded(h, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(h->device));
+    if (!h->d_y) TLRB_CUDA(cudaMalloc(&h->d_y, h->n * sizeof(double)));
+    TLRB_CUDA(cudaMemcpyAsync(h->d_z, x, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    apply_factor(h, h->d_z, h->d_y);
+    TLRB_CUDA(cudaMemcpyAsync(y, h->d_y, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    h->sync();
+    return TLRB_OK;
+  });
 }
 
 int32_t tlrb_solve(tlrb_handle* h, const double* rhs, double* x) {

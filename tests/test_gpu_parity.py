@@ -243,3 +243,16 @@ def test_max_rank_dense_fallback(tb, gold, max_rank, accs):
         assert (low == -1).any()                     # some tiles went dense
         assert low.max() <= max_rank
         assert st["max_rank"] <= max_rank
+
+
+@pytest.mark.parametrize("name", ["s120", "s300", "C1", "C2"])
+def test_sample_measurements_device(tb, gold, name):
+    """f2: z = L w on the device equals the reference's sample_measurements."""
+    if name not in gold["loglik"]:
+        pytest.skip("golden missing")
+    e = gold["loglik"][name]
+    locs = tb.generate_locations(e["n"], e["loc_seed"])
+    z = tb.sample_measurements(locs, tb.MaternParams(*e["theta"]), e["z_seed"])
+    ref = gold["z"][name]
+    # the reference assembles with its spline profile for n >= 256 (<= 1e-12 per entry)
+    np.testing.assert_allclose(z, ref, rtol=0, atol=1e-9 * np.abs(ref).max())
