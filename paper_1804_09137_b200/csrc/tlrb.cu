@@ -423,9 +423,49 @@ bool factor_tlr(tlrb_handle* h, double acc) {
     // K6 + K7: updates of (i, j), i > j > k, in job batches; a rank-0 panel
     // tile skips the update exactly like linalg.py:135
     std::vector<std::pair<int, int>> upd;
-    for (int j = k + 1; j < t; ++j)
-      for (int i = j + 1; i < t; ++i)
-        if (h->live(i, k) && h->live(j, k)) upd.push_back({i, j});
+    std::vector<GemmProb> dx, dy, dt;   // dense targets (A13): T_ij -= (L_ik L_jk^T)^T in place
+    {
+      double* tmpd = reinterpret_cast<double*>(h->ws);
+      size_t o = 0;
+      const size_t ws_doubles = h->ws_bytes / sizeof(double);
+      for (int j = k + 1; j < t; ++j)
+        for (int i = j + 1; i < t; ++i) {
+          if (!(h->live(i, k) && h->live(j, k))) continue;
+          if (!h->dn(i, j)) { upd.push_back({i, j}); continue; }
+          // a tile over the rank cap stays dense: no recompression, exact update
+          const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)];
+          const bool di = h->dn(i, k), dj = h->dn(j, k);
+          const int mi = h->sz[i], mj = h->sz[j], mk = h->sz[k];
+          double* T = h->Ut(i, j);
+          if (o + (size_t)nb * nb > ws_doubles) {
+            launch_gemm(dx, h->ar, h->stream); launch_gemm(dy, h->ar, h->stream); launch_gemm(dt, h->ar, h->stream);
+            dx.clear(); dy.clear(); dt.clear();
+            o = 0;
+          }
+          double* W = tmpd + o;
+          o += (size_t)nb * nb;
+          if (!di && !dj) {        // T -= U_jk (V_jk^T V_ik) U_ik^T
+            double* X = W;                          // kj x ki
+            double* Y = W + (size_t)kj * ki;        // mj x ki
+            dx.push_back({h->Vt(j, k), h->Vt(i, k), nullptr, X, kj, ki, mk, nb, nb, kj, kj, 1, 0, 0, 1.0, 0.0});
+            dy.push_back({h->Ut(j, k), X, nullptr, Y, mj, ki, kj, nb, kj, mj, mj, 0, 0, 0, 1.0, 0.0});
+            dt.push_back({Y, h->Ut(i, k), T, T, mj, mi, ki, mj, nb, nb, nb, 0, 1, 0, -1.0, 1.0});
+          } else if (di && !dj) {  // T -= U_jk (V_jk^T T_ik)
+            dx.push_back({h->Vt(j, k), h->Ut(i, k), nullptr, W, kj, mi, mk, nb, nb, kj, kj, 1, 0, 0, 1.0, 0.0});
+            dt.push_back({h->Ut(j, k), W, T, T, mj, mi, kj, nb, kj, nb, nb, 0, 0, 0, -1.0, 1.0});
+          } else if (!di && dj) {  // T -= (T_jk^T V_ik) U_ik^T
+            dx.push_back({h->Ut(j, k), h->Vt(i, k), nullptr, W, mj, ki, mk, nb, nb, mj, mj, 1, 0, 0, 1.0, 0.0});
+            dt.push_back({W, h->Ut(i, k), T, T, mj, mi, ki, mj, nb, nb, nb, 0, 1, 0, -1.0, 1.0});
+          } else {                 // T -= T_jk^T T_ik
+            dt.push_back({h->Ut(j, k), h->Ut(i, k), T, T, mj, mi, mk, nb, nb, nb, nb, 1, 0, 0, -1.0, 1.0});
+          }
+          const double a = di ? mk : ki, b = dj ? mk : kj;
+          h->work.add(2.0 * mi * mj * std::min(a, b) + 2.0 * mk * a * b, 8.0 * (2.0 * mi * mj + mk * (a + b)));
+        }
+      launch_gemm(dx, h->ar, h->stream);
+      launch_gemm(dy, h->ar, h->stream);
+      launch_gemm(dt, h->ar, h->stream);
+    }
     for (size_t c0 = 0; c0 < upd.size(); c0 += h->max_jobs) {
       const size_t c1 = std::min(upd.size(), c0 + h->max_jobs);
       std::vector<Job> jobs;
