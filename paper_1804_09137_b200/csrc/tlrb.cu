@@ -125,6 +125,11 @@ struct Job {
   int out_rank;
   bool dense_out;     // rank above max_rank: stored dense (L^T in Uout, ld ldu)
   uint64_t seed;
+  // factored recompression (compression.py:54-81): M is the K x K core,
+  // U_new = Qu u_core, V_new = Qv v_core are formed after compress_jobs
+  bool factored = false;
+  double* Qu = nullptr; double* Qv = nullptr; int mu = 0, nv = 0;
+  double* Ufin = nullptr; double* Vfin = nullptr;
 };
 
 void bind_slot(tlrb_handle* h, Job& J, int slot) {
@@ -466,12 +471,18 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_gemm(dy, h->ar, h->stream);
       launch_gemm(dt, h->ar, h->stream);
     }
+    static const double kFactoredFrac = getenv("TLRB_FACTORED_FRAC") ? atof(getenv("TLRB_FACTORED_FRAC")) : 0.15;
     for (size_t c0 = 0; c0 < upd.size(); c0 += h->max_jobs) {
       const size_t c1 = std::min(upd.size(), c0 + h->max_jobs);
       std::vector<Job> jobs;
       std::vector<GemmProb> gx, gy, gm, gm2;
       std::vector<CopyProb> cm;
       std::vector<SumsqProb> sq;
+      // factored-path launches
+      std::vector<GemmProb> fx, fy, fcore;
+      std::vector<CopyProb> fcp, fr;
+      std::vector<QrProb> fq;
+      std::vector<SumsqProb> fsq;
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
         const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], kij = h->rank[h->tid(i, j)];
@@ -480,6 +491,49 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         Job J{};
         const int slot = (int)(q - c0);
         bind_slot(h, J, slot);
+        const int K = kij + kj;
+        if (!di && !dj && !dij && K <= kFactoredFrac * std::min(mi, mj) &&
+            (h->max_rank <= 0 || K <= h->max_rank)) {
+          // stacked factors Us = [U_ij, -U_ik (V_ik^T V_jk)] (mi x K), Vs = [V_ij, U_jk] (mj x K)
+          double* Us = J.Y;
+          double* Vs = J.Y + (size_t)mi * K;
+          double* Qu = J.Q;
+          double* Qv = J.Q + (size_t)mi * K;
+          double* Tu = J.Om;                                // qr_kernel T: 16 (K + 16) doubles
+          double* Tv = J.Om + 16 * ((size_t)K + 16);
+          double* Xs = J.Om + 32 * ((size_t)K + 16);
+          double* uc = Xs + (size_t)ki * kj;
+          double* vc = uc + (size_t)K * K;
+          fx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, Xs, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
+          fcp.push_back({h->Ut(i, j), nb, Us, mi, mi, kij, 0, 1.0, 0, nullptr});
+          fy.push_back({h->Ut(i, k), Xs, nullptr, Us + (size_t)mi * kij, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, -1.0, 0.0});
+          fcp.push_back({h->Vt(i, j), nb, Vs, mj, mj, kij, 0, 1.0, 0, nullptr});
+          fcp.push_back({h->Ut(j, k), nb, Vs + (size_t)mj * kij, mj, mj, kj, 0, 1.0, 0, nullptr});
+          double* S = h->d_sums + 6 * slot;
+          fsq.push_back({Us, mi, mi, K, S + 2});
+          fsq.push_back({nullptr, 0, 0, 0, S + 3});
+          fsq.push_back({Vs, mj, mj, K, S + 4});
+          fsq.push_back({nullptr, 0, 0, 0, S + 5});
+          fq.push_back({Us, mi, Qu, mi, Tu, mi, K});
+          fq.push_back({Vs, mj, Qv, mj, Tv, mj, K});
+          // R^T (lower) of both, then core = Ru Rv^T = (Ru^T)^T (Rv^T)
+          fr.push_back({Us, mi, J.E, K, K, K, 1, 1.0, 1, nullptr});
+          fr.push_back({Vs, mj, J.Bt, K, K, K, 1, 1.0, 1, nullptr});
+          fcore.push_back({J.E, J.Bt, nullptr, J.M, K, K, K, K, K, K, K, 1, 0, 0, 1.0, 0.0});
+          J.m = J.n = K;
+          J.kind = 2;
+          J.s = K;
+          J.Uout = uc;
+          J.Vout = vc;
+          J.ldu = J.ldv = K;
+          J.factored = true;
+          J.Qu = Qu; J.Qv = Qv; J.mu = mi; J.nv = mj;
+          J.Ufin = h->Ut(i, j);
+          J.Vfin = h->Vt(i, j);
+          J.seed = 0;
+          jobs.push_back(J);
+          continue;
+        }
         J.m = mi;
         J.n = mj;
         J.kind = 2;
@@ -533,7 +587,25 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       // noise-floor norms (Y = U2 exists now; the tile's old factors are
       // only overwritten at the end of compress_jobs)
       launch_sumsq(sq, h->ar, h->stream);
+      // factored path: stacked factors, two Householder QRs, K x K core
+      launch_gemm(fx, h->ar, h->stream);
+      launch_copy(fcp, h->ar, h->stream);
+      launch_gemm(fy, h->ar, h->stream);
+      launch_sumsq(fsq, h->ar, h->stream);
+      launch_qr(fq, h->ar, h->stream);
+      launch_copy(fr, h->ar, h->stream);
+      launch_gemm(fcore, h->ar, h->stream);
       compress_jobs(h, jobs, acc);
+      {   // U_new = Qu u_core, V_new = Qv v_core (compression.py:81)
+        std::vector<GemmProb> fu;
+        for (const Job& J : jobs) {
+          if (!J.factored || !J.out_rank) continue;
+          const int kk = J.out_rank;
+          fu.push_back({J.Qu, J.Uout, nullptr, J.Ufin, J.mu, kk, J.m, J.mu, J.ldu, nb, nb, 0, 0, 0, 1.0, 0.0});
+          fu.push_back({J.Qv, J.Vout, nullptr, J.Vfin, J.nv, kk, J.n, J.nv, J.ldv, nb, nb, 0, 0, 0, 1.0, 0.0});
+        }
+        launch_gemm(fu, h->ar, h->stream);
+      }
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
         const double ki = h->dn(i, k) ? h->sz[k] : h->rank[h->tid(i, k)];
