@@ -61,6 +61,20 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
                          int32_t max_rank, int32_t device, int32_t* err);
 void tlrb_destroy(tlrb_handle* h);
 
+/* Multi-GPU (one process per GPU): 2D block-cyclic tile distribution over a
+ * P x Q process grid (P * Q == world), tile (i, j) on rank (i mod P) * Q +
+ * (j mod Q).  Per panel k: the owner of D_k factors it and broadcasts L_kk,
+ * owners of the panel tiles solve them and broadcast {U_ik, V_ik} (or the
+ * dense tile), owners of D_j / (i, j) apply their updates; ranks are
+ * all-reduced after every panel; log-det is all-reduced; the triangular
+ * solves reduce/broadcast one tile vector per step.  All collectives are NCCL
+ * on the handle's stream.  rank 0 creates the id with tlrb_nccl_unique_id
+ * (128 bytes) and shares it out of band (e.g. torch.distributed). */
+int32_t tlrb_nccl_unique_id(char* out, int32_t len);
+tlrb_handle* tlrb_create_dist(const double* xy, int64_t n, int32_t nb, int32_t max_rank,
+                              int32_t device, int32_t rank, int32_t world, int32_t P,
+                              int32_t Q, const char* nccl_id, int32_t* err);
+
 /* One Gaussian log-likelihood evaluation
  *   ll = -0.5 (n log 2pi + log|Sigma| + z' Sigma^-1 z)     (stats.py:112)
  * z: host pointer (n doubles).  acc == 0 -> dense mode, else TLR(acc).

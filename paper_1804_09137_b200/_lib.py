@@ -47,6 +47,9 @@ _IP = C.POINTER(C.c_int32)
 SIGNATURES = [
     ("tlrb_create", C.c_void_p, [_DP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _IP]),
     ("tlrb_destroy", None, [C.c_void_p]),
+    ("tlrb_nccl_unique_id", C.c_int32, [C.c_char_p, C.c_int32]),
+    ("tlrb_create_dist", C.c_void_p, [_DP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_char_p, _IP]),
     ("tlrb_loglik", C.c_int32, [C.c_void_p, _DP, C.c_double, C.c_double, C.c_double, C.c_double,
                                 C.c_double, _DP, _DP, _DP, C.POINTER(TlrbStats)]),
     ("tlrb_loglik_device", C.c_int32, [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,

@@ -149,14 +149,21 @@ class Handle:
     arenas reused across evaluations (one MLE run = one handle)."""
 
     def __init__(self, coords: np.ndarray, nb: int, max_rank: int = 0, ngpus: int = 1,
-                 device: int = 0):
+                 device: int = 0, dist: tuple | None = None):
+        """dist = (rank, world, P, Q, nccl_id_bytes): 2D block-cyclic multi-GPU
+        handle (one process per GPU); see `distributed_handle`."""
         self.lib = _lib.load()
         xy = np.ascontiguousarray(coords, dtype=np.float64)
         self.n = xy.shape[0]
         self.nb = int(min(nb, self.n))
         err = np.zeros(1, np.int32)
-        self.h = self.lib.tlrb_create(dptr(xy), self.n, self.nb, int(ngpus), int(max_rank or 0),
-                                      int(device), iptr(err))
+        if dist is None:
+            self.h = self.lib.tlrb_create(dptr(xy), self.n, self.nb, int(ngpus), int(max_rank or 0),
+                                          int(device), iptr(err))
+        else:
+            rank, world, P, Q, nid = dist
+            self.h = self.lib.tlrb_create_dist(dptr(xy), self.n, self.nb, int(max_rank or 0), int(device),
+                                               int(rank), int(world), int(P), int(Q), bytes(nid), iptr(err))
         if not self.h:
             raise (ValueError if err[0] == _lib.TLRB_ERR_ARG else DeviceError)(
                 f"tlrb_create failed (code {int(err[0])})")
@@ -247,6 +254,39 @@ class Handle:
         return r.reshape(tt, tt)
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = _lib.load().tlrb_nccl_unique_id(buf, 128)
+    if rc:
+        raise DeviceError("ncclGetUniqueId failed")
+    return buf.raw
+
+
+def distributed_handle(coords, nb: int, max_rank: int = 0, P: int | None = None,
+                       Q: int | None = None, device: int | None = None) -> Handle:
+    """Handle over all ranks of the default torch.distributed group (one
+    process per GPU): 2D block-cyclic tiles on a P x Q grid.
+    Single process without torch.distributed: world = 1."""
+    from .dist import grid_shape
+    try:
+        import torch.distributed as tdist
+        on = tdist.is_available() and tdist.is_initialized()
+    except ImportError:
+        on = False
+    rank, world = (tdist.get_rank(), tdist.get_world_size()) if on else (0, 1)
+    if P is None or Q is None:
+        P, Q = grid_shape(world)
+    nid = nccl_unique_id() if rank == 0 else bytes(128)
+    if on and world > 1:
+        obj = [nid]
+        tdist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    if device is None:
+        import os
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    return Handle(coords, nb, max_rank, device=device, dist=(rank, world, P, Q, nid))
+
+
 _HANDLES: dict = {}
 
 
@@ -256,7 +296,10 @@ def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus) -> Handle:
     if h is None or h[0] is not coords:
         if len(_HANDLES) > 8:
             _HANDLES.clear()
-        h = (coords, Handle(coords, nb, max_rank or 0, ngpus))
+        if ngpus and ngpus > 1:   # one process per GPU under torch.distributed
+            h = (coords, distributed_handle(coords, nb, max_rank or 0))
+        else:
+            h = (coords, Handle(coords, nb, max_rank or 0))
         _HANDLES[key] = h
     return h[1]
 

@@ -25,7 +25,7 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC, *FLAGS, *map(str, SRC), "-o", str(OUT)]
+    cmd = [NVCC, *FLAGS, *map(str, SRC), "-o", str(OUT), "-lnccl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

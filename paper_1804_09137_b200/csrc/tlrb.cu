@@ -25,6 +25,7 @@
 //   ws     : per-job compression workspace slots (M, E, Y, Q, Omega, B^T, V)
 #include "common.cuh"
 #include "../../include/tlrb200.h"
+#include <nccl.h>
 #include <cmath>
 #include <string>
 #include <chrono>
@@ -91,6 +92,16 @@ struct tlrb_handle {
   Flops work;
   int retries = 0, max_sweeps = 0;
 
+  // 2D block-cyclic distribution: tile (i, j) lives on rank
+  // (i mod P) * Q + (j mod Q); comm == nullptr -> single-GPU path
+  int drank = 0, dworld = 1, P = 1, Q = 1;
+  ncclComm_t comm = nullptr;
+  int* d_ibuf = nullptr;         // int all-reduce scratch (2 * ntile + 4)
+  double* d_acc = nullptr;       // distributed solve accumulator (n)
+  bool dist() const { return comm != nullptr; }
+  int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
+  bool own(int i, int j) const { return !comm || owner(i, j) == drank; }
+
   size_t tid(int i, int j) const { return (size_t)i * (i - 1) / 2 + j; }
   bool dn(int i, int j) const { return dense[tid(i, j)] != 0; }
   bool live(int i, int j) const { return dense[tid(i, j)] || rank[tid(i, j)] > 0; }
@@ -112,6 +123,45 @@ bool trace_on() {
 }
 double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+#define TLRB_NCCL(call)                                                              \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess) throw CudaError(cudaErrorUnknown, ncclGetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+
+// all ranks learn every tile's rank / dense flag (owners contribute, others 0)
+void sync_ranks(tlrb_handle* h) {
+  if (!h->dist()) return;
+  const size_t nt = h->rank.size();
+  std::vector<int> buf(2 * nt, 0);
+  for (int i = 1; i < h->t; ++i)
+    for (int j = 0; j < i; ++j)
+      if (h->own(i, j)) {
+        buf[h->tid(i, j)] = h->rank[h->tid(i, j)];
+        buf[nt + h->tid(i, j)] = h->dense[h->tid(i, j)];
+      }
+  if (nt) {
+    TLRB_CUDA(cudaMemcpyAsync(h->d_ibuf, h->ar.put(buf, h->stream), 2 * nt * sizeof(int), cudaMemcpyDeviceToDevice,
+                              h->stream));
+    TLRB_NCCL(ncclAllReduce(h->d_ibuf, h->d_ibuf, 2 * nt, ncclInt32, ncclSum, h->comm, h->stream));
+    TLRB_CUDA(cudaMemcpyAsync(buf.data(), h->d_ibuf, 2 * nt * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  }
+  h->sync();
+  for (size_t q = 0; q < nt; ++q) {
+    h->rank[q] = buf[q];
+    h->dense[q] = (char)buf[nt + q];
+  }
+}
+
+void bcast(tlrb_handle* h, double* buf, size_t count, int root) {
+  if (!h->dist() || !count) return;
+  TLRB_NCCL(ncclBroadcast(buf, buf, count, ncclFloat64, root, h->comm, h->stream));
+}
+
+__global__ void axpy_kernel(double* y, const double* x, double a, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] += a * x[i];
 }
 
 // ------------------------------------------------------------ compression
@@ -246,10 +296,10 @@ int sketch_guess(int prev_rank, int n) {
 void generate(tlrb_handle* h, double nugget, bool dense_lower) {
   std::vector<GenTile> tiles;
   for (int i = 0; i < h->t; ++i) {
-    tiles.push_back({h->D(i), h->nb, h->off[i], h->sz[i], h->off[i], h->sz[i], nugget});
+    if (h->own(i, i)) tiles.push_back({h->D(i), h->nb, h->off[i], h->sz[i], h->off[i], h->sz[i], nugget});
     if (dense_lower)
       for (int j = 0; j < i; ++j)  // L_ij^T: rows = tile j points, cols = tile i points
-        tiles.push_back({h->Ut(i, j), h->nb, h->off[j], h->sz[j], h->off[i], h->sz[i], 0.0});
+        if (h->own(i, j)) tiles.push_back({h->Ut(i, j), h->nb, h->off[j], h->sz[j], h->off[i], h->sz[i], 0.0});
   }
   launch_gen_tiles(tiles, h->dx, h->dy, h->mp, h->ar, h->stream);
   for (int i = 0; i < h->t; ++i) {
@@ -262,7 +312,8 @@ void generate(tlrb_handle* h, double nugget, bool dense_lower) {
 void compress_all(tlrb_handle* h, double acc) {
   std::vector<std::pair<int, int>> all;
   for (int i = 1; i < h->t; ++i)
-    for (int j = 0; j < i; ++j) all.push_back({i, j});
+    for (int j = 0; j < i; ++j)
+      if (h->own(i, j)) all.push_back({i, j});
   // far tiles first (small ranks), near-diagonal last
   for (size_t c0 = 0; c0 < all.size(); c0 += h->max_jobs) {
     const size_t c1 = std::min(all.size(), c0 + h->max_jobs);
@@ -295,10 +346,15 @@ void compress_all(tlrb_handle* h, double acc) {
       h->work.add(4.0 * m * n * k, 8.0 * m * n + 8.0 * k * (m + n));
     }
   }
+  sync_ranks(h);
 }
 
 // ------------------------------------------------------------------ POTRF
 void potrf(tlrb_handle* h, int k) {
+  if (!h->own(k, k)) {   // L_kk arrives from its owner
+    bcast(h, h->D(k), (size_t)h->nb * h->nb, h->owner(k, k));
+    return;
+  }
   const int n = h->sz[k];
   double* A = h->D(k);
   for (int r0 = 0; r0 < n; r0 += kPotrfBlock) {
@@ -315,11 +371,35 @@ void potrf(tlrb_handle* h, int k) {
   }
   const double nn = n;
   h->work.add(nn * nn * nn / 3.0, 16.0 * nn * nn);
+  bcast(h, h->D(k), (size_t)h->nb * h->nb, h->owner(k, k));
+}
+
+// panel tiles (i, k), i > k, from their owners to every rank
+void bcast_panel(tlrb_handle* h, int k, bool dense_mode) {
+  if (!h->dist()) return;
+  TLRB_NCCL(ncclGroupStart());
+  for (int i = k + 1; i < h->t; ++i) {
+    const int root = h->owner(i, k);
+    if (dense_mode || h->dn(i, k)) {
+      bcast(h, h->Ut(i, k), (size_t)h->nb * h->sz[i], root);
+    } else {
+      const size_t r = h->rank[h->tid(i, k)];
+      bcast(h, h->Ut(i, k), (size_t)h->nb * r, root);
+      bcast(h, h->Vt(i, k), (size_t)h->nb * r, root);
+    }
+  }
+  TLRB_NCCL(ncclGroupEnd());
 }
 
 bool check_npd(tlrb_handle* h) {
   int info[3];
-  TLRB_CUDA(cudaMemcpyAsync(info, h->d_info, sizeof info, cudaMemcpyDeviceToHost, h->stream));
+  const int* src = h->d_info;
+  if (h->dist()) {   // the failing tile's owner reported it; everyone stops
+    int* tot = h->d_ibuf + 2 * h->rank.size();
+    TLRB_NCCL(ncclAllReduce(h->d_info, tot, 3, ncclInt32, ncclSum, h->comm, h->stream));
+    src = tot;
+  }
+  TLRB_CUDA(cudaMemcpyAsync(info, src, sizeof info, cudaMemcpyDeviceToHost, h->stream));
   h->sync();
   if (info[0]) {
     h->err_tile = info[1];
@@ -339,17 +419,21 @@ bool factor_dense(tlrb_handle* h) {
   for (int k = 0; k < t; ++k) {
     potrf(h, k);
     std::vector<TrsmProb> tp;
-    for (int i = k + 1; i < t; ++i) tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
+    for (int i = k + 1; i < t; ++i)
+      if (h->own(i, k)) tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
     launch_trsm(tp, false, h->ar, h->stream);
+    bcast_panel(h, k, true);
     std::vector<GemmProb> gp;
     const double nk = h->sz[k];
     for (int j = k + 1; j < t; ++j) {
       // D_j -= L_jk L_jk^T = T_jk^T T_jk
-      gp.push_back({h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
-                    nb, 1, 0, 1, -1.0, 1.0});
+      if (h->own(j, j))
+        gp.push_back({h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
+                      nb, 1, 0, 1, -1.0, 1.0});
       h->work.add(nk * h->sz[j] * h->sz[j], 8.0 * (2.0 * nk * h->sz[j] + 2.0 * h->sz[j] * h->sz[j]));
       // T_ij -= T_jk^T T_ik
       for (int i = j + 1; i < t; ++i) {
+        if (!h->own(i, j)) continue;
         gp.push_back({h->Ut(j, k), h->Ut(i, k), h->Ut(i, j), h->Ut(i, j), h->sz[j], h->sz[i], h->sz[k], nb,
                       nb, nb, nb, 1, 0, 0, -1.0, 1.0});
         h->work.add(2.0 * nk * h->sz[i] * h->sz[j],
@@ -374,6 +458,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
     std::vector<TrsmProb> tp;
     for (int i = k + 1; i < t; ++i) {
       const double nk = h->sz[k];
+      if (!h->own(i, k)) continue;
       if (h->dn(i, k)) {
         tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
         h->work.add(nk * nk * h->sz[i], 8.0 * (nk * nk / 2 + 2.0 * nk * h->sz[i]));
@@ -385,6 +470,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
     }
     launch_trsm(tp, false, h->ar, h->stream);
     if (check_npd(h)) return false;
+    bcast_panel(h, k, false);
     // K5: D_j -= U_jk (V_jk^T V_jk) U_jk^T  (dense panel tile: D_j -= T_jk^T T_jk)
     {
       std::vector<GemmProb> g1, g2, g3;
@@ -392,6 +478,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       const size_t ws_doubles = h->ws_bytes / sizeof(double);
       for (int j = k + 1; j < t; ++j) {
         const double nj = h->sz[j];
+        if (!h->own(j, j)) continue;
         if (h->dn(j, k)) {
           g3.push_back({h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
                         nb, 1, 0, 1, -1.0, 1.0});
@@ -435,7 +522,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       const size_t ws_doubles = h->ws_bytes / sizeof(double);
       for (int j = k + 1; j < t; ++j)
         for (int i = j + 1; i < t; ++i) {
-          if (!(h->live(i, k) && h->live(j, k))) continue;
+          if (!(h->live(i, k) && h->live(j, k)) || !h->own(i, j)) continue;
           if (!h->dn(i, j)) { upd.push_back({i, j}); continue; }
           // a tile over the rank cap stays dense: no recompression, exact update
           const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)];
@@ -621,12 +708,16 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         h->dense[h->tid(i, j)] = J.dense_out;
       }
     }
+    sync_ranks(h);   // every rank learns the new ranks before the next panel broadcast
   }
   return !check_npd(h);
 }
 
 // ------------------------------------------------------------ y = L x
 // (sample_measurements, stats.py:115-133: z = L w tile by tile)
+void add_tile_times(tlrb_handle* h, int i, int j, const double* x, double* acc, bool transpose,
+                    std::vector<GemmProb>& g1, std::vector<GemmProb>& g2);
+
 __global__ void tril_kernel(double* A, int ld, int n) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
     const int r = e % n, c = e / n;
@@ -636,6 +727,29 @@ __global__ void tril_kernel(double* A, int ld, int n) {
 
 void apply_factor(tlrb_handle* h, const double* dx, double* dy) {
   const int t = h->t, nb = h->nb;
+  if (h->dist()) {   // owned contributions, then one sum all-reduce
+    TLRB_CUDA(cudaMemsetAsync(dy, 0, h->n * sizeof(double), h->stream));
+    for (int i = 0; i < t; ++i) {
+      if (!h->own(i, i)) continue;
+      tril_kernel<<<64, 256, 0, h->stream>>>(h->D(i), nb, h->sz[i]);
+      post_launch();
+    }
+    std::vector<GemmProb> g0, g1, g2;
+    for (int i = 0; i < t; ++i)
+      if (h->own(i, i))
+        g0.push_back({h->D(i), dx + h->off[i], dy + h->off[i], dy + h->off[i], h->sz[i], 1, h->sz[i], nb,
+                      h->sz[i], h->sz[i], h->sz[i], 0, 0, 0, 1.0, 1.0});
+    launch_gemm(g0, h->ar, h->stream);
+    for (int j = 0; j < t; ++j) {
+      g1.clear(); g2.clear();
+      for (int i = j + 1; i < t; ++i)
+        if (h->own(i, j)) add_tile_times(h, i, j, dx + h->off[j], dy + h->off[i], false, g1, g2);
+      launch_gemm(g1, h->ar, h->stream);
+      launch_gemm(g2, h->ar, h->stream);
+    }
+    TLRB_NCCL(ncclAllReduce(dy, dy, h->n, ncclFloat64, ncclSum, h->comm, h->stream));
+    return;
+  }
   for (int i = 0; i < t; ++i) {   // the diagonal factors' upper parts are stale: clear them
     tril_kernel<<<64, 256, 0, h->stream>>>(h->D(i), nb, h->sz[i]);
     post_launch();
@@ -668,8 +782,68 @@ void apply_factor(tlrb_handle* h, const double* dx, double* dy) {
   }
 }
 
+// ------------------------------------------------ distributed solves (8(e))
+// Forward: for each tile column j, the contributions sum_i L_ji y_i
+// accumulated by the owners of (j, i) are reduced onto the owner of D_j,
+// which solves y_j and broadcasts it; owners of (i, j), i > j, then add
+// L_ij y_j into their accumulators.  Every rank ends with the full y.
+void add_tile_times(tlrb_handle* h, int i, int j, const double* x, double* acc, bool transpose,
+                    std::vector<GemmProb>& g1, std::vector<GemmProb>& g2) {
+  const int nb = h->nb;
+  // transpose == false: acc_i += L_ij x_j ; true: acc_j += L_ij^T x_i
+  if (h->factor_mode == 1 || h->dn(i, j)) {
+    if (!transpose)
+      g1.push_back({h->Ut(i, j), x, acc, acc, h->sz[i], 1, h->sz[j], nb, h->sz[j], h->sz[i], h->sz[i], 1, 0, 0,
+                    1.0, 1.0});
+    else
+      g1.push_back({h->Ut(i, j), x, acc, acc, h->sz[j], 1, h->sz[i], nb, h->sz[i], h->sz[j], h->sz[j], 0, 0, 0,
+                    1.0, 1.0});
+    return;
+  }
+  const int r = h->rank[h->tid(i, j)];
+  if (!r) return;
+  double* w = h->d_w + (size_t)(transpose ? j : i) * nb;
+  if (!transpose) {
+    g1.push_back({h->Vt(i, j), x, nullptr, w, r, 1, h->sz[j], nb, h->sz[j], r, r, 1, 0, 0, 1.0, 0.0});
+    g2.push_back({h->Ut(i, j), w, acc, acc, h->sz[i], 1, r, nb, r, h->sz[i], h->sz[i], 0, 0, 0, 1.0, 1.0});
+  } else {
+    g1.push_back({h->Ut(i, j), x, nullptr, w, r, 1, h->sz[i], nb, h->sz[i], r, r, 1, 0, 0, 1.0, 0.0});
+    g2.push_back({h->Vt(i, j), w, acc, acc, h->sz[j], 1, r, nb, r, h->sz[j], h->sz[j], 0, 0, 0, 1.0, 1.0});
+  }
+}
+
+void solve_dist(tlrb_handle* h, bool backward) {
+  const int t = h->t, nb = h->nb;
+  cudaStream_t s = h->stream;
+  TLRB_CUDA(cudaMemsetAsync(h->d_acc, 0, h->n * sizeof(double), s));
+  for (int q = 0; q < t; ++q) {
+    const int j = backward ? t - 1 - q : q;
+    double* zj = h->d_z + h->off[j];
+    double* aj = h->d_acc + h->off[j];
+    const int root = h->owner(j, j);
+    TLRB_NCCL(ncclReduce(aj, aj, h->sz[j], ncclFloat64, ncclSum, root, h->comm, s));
+    if (h->own(j, j)) {
+      axpy_kernel<<<4, 256, 0, s>>>(zj, aj, -1.0, h->sz[j]);
+      post_launch();
+      launch_trsm({TrsmProb{h->D(j), nb, zj, h->sz[j], h->sz[j], 1}}, backward, h->ar, s);
+    }
+    bcast(h, zj, h->sz[j], root);
+    std::vector<GemmProb> g1, g2;
+    if (!backward) {
+      for (int i = j + 1; i < t; ++i)
+        if (h->own(i, j)) add_tile_times(h, i, j, zj, h->d_acc + h->off[i], false, g1, g2);
+    } else {
+      for (int l = 0; l < j; ++l)
+        if (h->own(j, l)) add_tile_times(h, j, l, zj, h->d_acc + h->off[l], true, g1, g2);
+    }
+    launch_gemm(g1, h->ar, s);
+    launch_gemm(g2, h->ar, s);
+  }
+}
+
 // ------------------------------------------------------------------ solves
 void forward_solve(tlrb_handle* h) {
+  if (h->dist()) { solve_dist(h, false); return; }
   const int t = h->t, nb = h->nb;
   for (int j = 0; j < t; ++j) {
     double* yj = h->d_z + h->off[j];
@@ -694,6 +868,7 @@ void forward_solve(tlrb_handle* h) {
 }
 
 void backward_solve(tlrb_handle* h) {
+  if (h->dist()) { solve_dist(h, true); return; }
   const int t = h->t, nb = h->nb;
   for (int i = t - 1; i >= 0; --i) {
     double* xi = h->d_z + h->off[i];
@@ -738,6 +913,7 @@ int factorize(tlrb_handle* h, double th1, double th2, double th3, double nugget,
   h->err_tile = h->err_pivot = -1;
   h->factor_mode = 0;
   TLRB_CUDA(cudaMemsetAsync(h->d_info, 0, 3 * sizeof(int), s));
+  TLRB_CUDA(cudaMemsetAsync(h->d_logdiag, 0, h->n * sizeof(double), s));
   TLRB_CUDA(cudaEventRecord(h->ev[0], s));
   const bool dense = acc == 0.0;
   generate(h, nugget, dense);
@@ -773,6 +949,8 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
   forward_solve(h);
   launch_dot(h->d_z, (int)h->n, h->d_scal + 1, s);
   launch_sum_log(h->d_logdiag, (int)h->n, h->d_scal, s);
+  if (h->dist())   // log-det: owners of the diagonal tiles hold the partial sums
+    TLRB_NCCL(ncclAllReduce(h->d_scal, h->d_scal, 1, ncclFloat64, ncclSum, h->comm, s));
   TLRB_CUDA(cudaEventRecord(h->ev[4], s));
   double sc[2];
   TLRB_CUDA(cudaMemcpyAsync(sc, h->d_scal, sizeof sc, cudaMemcpyDeviceToHost, s));
@@ -908,10 +1086,52 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
   return h;
 }
 
+int32_t tlrb_nccl_unique_id(char* out, int32_t len) {
+  if (!out || len < (int32_t)sizeof(ncclUniqueId)) return TLRB_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return TLRB_ERR_CUDA;
+  memcpy(out, &id, sizeof id);
+  return TLRB_OK;
+}
+
+tlrb_handle* tlrb_create_dist(const double* xy, int64_t n, int32_t nb, int32_t max_rank, int32_t device,
+                              int32_t rank, int32_t world, int32_t P, int32_t Q, const char* nccl_id,
+                              int32_t* err) {
+  if (err) *err = TLRB_OK;
+  if (!nccl_id || world < 1 || rank < 0 || rank >= world || P < 1 || Q < 1 || P * Q != world) {
+    if (err) *err = TLRB_ERR_ARG;
+    return nullptr;
+  }
+  tlrb_handle* h = tlrb_create(xy, n, nb, 1, max_rank, device, err);
+  if (!h) return nullptr;
+  const int rc = guarded(h, [&]() -> int {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    h->drank = rank;
+    h->dworld = world;
+    h->P = P;
+    h->Q = Q;
+    TLRB_NCCL(ncclCommInitRank(&h->comm, world, id, rank));
+    TLRB_CUDA(cudaMalloc(&h->d_ibuf, (2 * h->rank.size() + 8) * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_acc, h->n * sizeof(double)));
+    return TLRB_OK;
+  });
+  if (rc != TLRB_OK) {
+    if (err) *err = rc;
+    fprintf(stderr, "tlrb_create_dist: %s\n", h->msg.c_str());
+    tlrb_destroy(h);
+    return nullptr;
+  }
+  return h;
+}
+
 void tlrb_destroy(tlrb_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->d_ibuf) cudaFree(h->d_ibuf);
+  if (h->d_acc) cudaFree(h->d_acc);
   void* ptrs[] = {h->dx, h->dy, h->diag, h->U, h->V, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
                   h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_y, h->d_ux, h->d_uy,
                   h->d_pred, h->d_partial};

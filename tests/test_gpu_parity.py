@@ -256,3 +256,25 @@ def test_sample_measurements_device(tb, gold, name):
     ref = gold["z"][name]
     # the reference assembles with its spline profile for n >= 256 (<= 1e-12 per entry)
     np.testing.assert_allclose(z, ref, rtol=0, atol=1e-9 * np.abs(ref).max())
+
+
+def test_distributed_path_world1(tb, gold):
+    """The NCCL block-cyclic path (tlrb_create_dist) at world = 1 gives the
+    single-GPU results (same arithmetic; solves go through reduce/broadcast)."""
+    e = gold["loglik"]["C1"]
+    locs = tb.generate_locations(e["n"], e["loc_seed"])
+    p = tb.MaternParams(*e["theta"])
+    z = gold["z"]["C1"]
+    hd = tb.api.distributed_handle(locs.coords, e["nb"])
+    hs = tb.Handle(locs.coords, e["nb"])
+    for acc in (None, 1e-9):
+        a = hd.loglik(z, p, acc)
+        b = hs.loglik(z, p, acc)
+        np.testing.assert_allclose(a, b, rtol=1e-12)
+        ref = e["modes"]["dense" if acc is None else "tlr:1e-09"]["ll"]
+        assert abs(a[0] - ref) <= (1e-10 if acc is None else 1e-8) * abs(ref)
+        x = np.random.default_rng(0).standard_normal(e["n"])
+        np.testing.assert_allclose(hd.solve(x), hs.solve(x), rtol=1e-10, atol=1e-10)
+        np.testing.assert_allclose(hd.apply_factor(x), hs.apply_factor(x), rtol=1e-12, atol=1e-12)
+    hd.close()
+    hs.close()
