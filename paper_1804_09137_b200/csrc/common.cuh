@@ -111,6 +111,7 @@ struct JacobiProb {        // one-sided Jacobi on the columns of X (m x s)
   int* rank_out;           // truncation rank (compression.py:26-36 rule)
   int* sweeps_out;
   int m, s;
+  long long* prof = nullptr;   // optional phase cycle counters (debug)
 };
 
 // ----------------------------------------------------------- small helpers

@@ -37,8 +37,13 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
+constexpr bool kPipelined = false;   // per-column producer/consumer barriers (experimental)
+
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // round-robin tournament over nplayers (even): match idx of round r
@@ -51,6 +56,24 @@ __device__ __forceinline__ void match(int r, int idx, int np, int& p, int& q) {
     p = (r + idx) % rot;
     q = (r - idx + rot) % rot;
   }
+}
+
+// 1/sqrt(x) and 1/x for normal positive / nonzero x: approximate MUFU seed
+// (rsqrt.approx.f64 / rcp.approx.ftz.f64, ~2^-22) + two Newton steps
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
 }
 
 // Cross rotation of a register-resident column xa (rows lane + 32 i) with a
@@ -68,10 +91,14 @@ __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL]
   const double ga = wsum(g0 + g1);
   if (ga == 0.0 || ga * ga <= (tol * tol) * (al * be)) return false;
   // t = sign(zeta)/(|zeta| + sqrt(1+zeta^2)), zeta = (be-al)/(2ga), written
-  // with one division: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2))
+  // with one reciprocal: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)).  The
+  // rotation only has to be orthogonal to ~u, so hardware rsqrt / rcp seeds
+  // + Newton steps replace IEEE sqrt / div (75-134 cycle latencies).
   const double d = be - al, g2 = 2.0 * ga;
-  const double t = (d >= 0.0 ? g2 : -g2) / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-  const double c = rsqrt(fma(t, t, 1.0));
+  const double q2 = fma(d, d, g2 * g2);
+  const double hyp = q2 * fast_rsqrt(q2);
+  const double t = (d >= 0.0 ? g2 : -g2) * fast_rcp(fabs(d) + hyp);
+  const double c = fast_rsqrt(fma(t, t, 1.0));
   const double sn = c * t;
 #pragma unroll
   for (int i = 0; i < RPL; ++i) {
@@ -198,11 +225,15 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
     }
   };
 
+  long long c_load = 0, c_within = 0, c_cross = 0, c_store = 0, c_sync = 0, c_conv = 0;
+  long long tt = clock64();
+  auto tick = [&](long long& acc) { const long long now = clock64(); acc += now - tt; tt = now; };
   if (s > 1) {
     for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
       bool any = false;
       for (int r = 0; r < np - 1; ++r) {
-        for (int idx = crank; idx < np / 2; idx += CL) {
+        for (int slot = crank; slot < np / 2; slot += CL) {
+          const int idx = (slot + r) % (np / 2);   // the dummy pairing visits every CTA
           int I, J;
           match(r, idx, np, I, J);
           if (I >= nblk) { const int t = I; I = J; J = t; }   // I real, J maybe dummy
@@ -214,6 +245,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
           norms_of(S0, nrm[0]);
           if (realJ) norms_of(S1, nrm[1]);
           __syncthreads();
+          tick(c_load);
           const int ncI = min(B, s - I * B);
           const int ncJ = realJ ? min(B, s - J * B) : 0;
           if (r == 0) {   // pairs inside blocks I and J, concurrently on two warp halves
@@ -221,6 +253,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
             else if (realJ && warp < B) within(S1, nrm[1], ncJ, B / 2, 2, any);
             __syncthreads();
           }
+          tick(c_within);
           if (realJ && warp < B) {
             // warp w keeps column w of block I in registers and meets the J
             // columns in order w, w+1, ...; the cross warps meet at a named
@@ -233,7 +266,9 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
             bool dirty = false;
             for (int rr = 0; rr < B; ++rr) {
               const int q = (p + rr) % B;
-              named_bar(3, B * 32);   // round rr: all cross warps are past round rr-1
+              // column q was used in round rr-1 by warp p+1: wait on q's
+              // producer/consumer barrier (ids 1..B, two warps each)
+              if (kPipelined) { if (rr > 0) named_bar(1 + q, 64); } else { named_bar(15, B * 32); }
               if (p < ncI && q < ncJ) {
                 ld_col(xb, S1 + q * m);
                 double be = nrm[1][q];
@@ -244,16 +279,21 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
                   if (lane == 0) nrm[1][q] = be;
                 }
               }
+              // hand column q to warp p-1 (its round rr+1); bar.arrive orders the stores
+              if (kPipelined && rr < B - 1) named_arrive(1 + q, 64);
             }
             if (dirty) st_col(xa, S0 + p * m);
           }
           __syncthreads();
+          tick(c_cross);
           store(S0, I);
           if (realJ) store(S1, J);
           __syncthreads();
+          tick(c_store);
         }
         __threadfence();
         cl.sync();
+        tick(c_sync);
       }
       // cluster-wide convergence decision through distributed shared memory
       if (threadIdx.x == 0) rot_flag = 0;
@@ -268,8 +308,14 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
       __syncthreads();
       const bool more = S0[0] != 0.0;
       cl.sync();   // everyone has read the flags before they are reset
+      tick(c_conv);
       if (!more) break;
     }
+  }
+  if (P.prof && threadIdx.x == 0) {
+    long long* q = P.prof + 8 * crank;
+    q[0] = c_load; q[1] = c_within; q[2] = c_cross; q[3] = c_store; q[4] = c_sync; q[5] = c_conv;
+    q[6] = sweeps;
   }
   if (crank != 0) return;
   if (threadIdx.x == 0) *P.sweeps_out = sweeps;
@@ -387,13 +433,13 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     // nblk = 2 CL blocks of width ceil(smax / 2CL), even, <= B
     int Bg = (smax + 2 * CL - 1) / (2 * CL);
     Bg = std::min(B, std::max(2, (Bg + 1) & ~1));
-    const size_t smem = std::max((size_t)2 * Bg * mmax * 8, (size_t)smax * 12 + 64);
     // rows per lane and the thread bound (registers: 2 RPL doubles per lane)
     auto kern = mmax <= 512 ? jacobi_cluster_kernel<16, 512>
               : mmax <= 768 ? jacobi_cluster_kernel<24, 512>
               : mmax <= 1024 ? jacobi_cluster_kernel<32, 256> : jacobi_cluster_kernel<64, 128>;
-    const int bmax = mmax <= 768 ? 16 : mmax <= 1024 ? 8 : 4;
+    const int bmax = mmax <= 768 ? 14 : mmax <= 1024 ? 8 : 4;
     if (Bg > bmax) Bg = bmax;
+    const size_t smem = std::max((size_t)2 * Bg * mmax * 8, (size_t)smax * 12 + 64);
     TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     double by = 0;

@@ -251,7 +251,24 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
       jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, h->d_aux + 3 * j, acc, h->d_rank + j,
                     h->d_sweeps + j, J.n, J.s});
     }
+    static long long* d_prof = nullptr;
+    const bool prof = getenv("TLRB_JACOBI_PROF") != nullptr;
+    if (prof) {
+      if (!d_prof) TLRB_CUDA(cudaMalloc(&d_prof, 16 * 8 * sizeof(long long)));
+      TLRB_CUDA(cudaMemsetAsync(d_prof, 0, 16 * 8 * sizeof(long long), s));
+      for (auto& q : jp) q.prof = nullptr;
+      jp[0].prof = d_prof;   // first problem only (one tile in tools/one_tile.py)
+    }
     launch_jacobi(jp, h->ar, s);
+    if (prof) {
+      long long hp[16 * 8];
+      TLRB_CUDA(cudaMemcpyAsync(hp, d_prof, sizeof hp, cudaMemcpyDeviceToHost, s));
+      h->sync();
+      for (int c = 0; c < 16; ++c)
+        if (hp[8 * c + 6])
+          fprintf(stderr, "[jacobi-prof] cta %d load %lld within %lld cross %lld store %lld sync %lld conv %lld sweeps %lld\n",
+                  c, hp[8 * c], hp[8 * c + 1], hp[8 * c + 2], hp[8 * c + 3], hp[8 * c + 4], hp[8 * c + 5], hp[8 * c + 6]);
+    }
   }
   std::vector<int> rk(nj), sw(nj);
   TLRB_CUDA(cudaMemcpyAsync(rk.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
