@@ -379,3 +379,63 @@ def predict(known_xy, z, unknown_xy, theta, nb, acc=None):
     D, L, _ = cholesky(*assemble(known_xy, theta, nb, acc), acc)
     w = backward_solve(D, L, n, nb, forward_solve(D, L, n, nb, z))
     return matern_block(unknown_xy, known_xy, theta) @ w
+
+
+# --------------------------------------------------------------------------
+# bounded Nelder-Mead MLE (stats.py:144-251) — checker for the device driver
+# --------------------------------------------------------------------------
+def mle_fit(objective, bounds, theta0=None, max_iterations=100, tol=1e-9):
+    """Returns (best theta, best loglik, iterations, converged, trace of thetas)."""
+    lo = [b[0] for b in bounds]
+    hi = [b[1] for b in bounds]
+    clamp = lambda x: np.array([min(max(x[d], lo[d]), hi[d]) for d in range(len(x))])
+    thetas = []
+
+    def neg(x):
+        thetas.append(tuple(float(v) for v in x))
+        ll = objective(x)
+        return -ll if math.isfinite(ll) else math.inf
+
+    x0 = clamp(np.asarray(theta0 if theta0 is not None else [math.sqrt(a * b) for a, b in bounds],
+                          dtype=float))
+    verts = [x0.copy()]
+    for d in range(x0.size):                              # stats.py:148-158
+        step = 0.25 * x0[d]
+        v = x0.copy()
+        if v[d] + step > hi[d]:
+            step = -step
+        v[d] = min(max(v[d] + step, lo[d]), hi[d])
+        verts.append(v)
+    fv = [neg(v) for v in verts]
+    it, conv = 0, False
+    while it < max_iterations:                            # stats.py:206-237
+        o = np.argsort(fv, kind="stable")
+        verts = [verts[k] for k in o]
+        fv = [fv[k] for k in o]
+        a, b = fv[0], fv[-1]
+        spread = (2.0 * abs(b - a) / (abs(b) + abs(a) + 1e-300)
+                  if math.isfinite(a) and math.isfinite(b) else math.inf)
+        if spread <= tol:
+            conv = True
+            break
+        it += 1
+        c = np.mean(verts[:-1], axis=0)
+        xr = clamp(c + (c - verts[-1]))
+        fr = neg(xr)
+        if fv[0] <= fr < fv[-2]:
+            verts[-1], fv[-1] = xr, fr
+        elif fr < fv[0]:
+            xe = clamp(c + 2.0 * (xr - c))
+            fe = neg(xe)
+            verts[-1], fv[-1] = (xe, fe) if fe < fr else (xr, fr)
+        else:
+            xc = clamp(c + 0.5 * ((xr if fr < fv[-1] else verts[-1]) - c))
+            fc = neg(xc)
+            if fc < min(fr, fv[-1]):
+                verts[-1], fv[-1] = xc, fc
+            else:
+                for k in range(1, len(verts)):
+                    verts[k] = clamp(verts[0] + 0.5 * (verts[k] - verts[0]))
+                    fv[k] = neg(verts[k])
+    best = int(np.argmin(fv))
+    return verts[best], -fv[best], it, conv, thetas

@@ -382,16 +382,27 @@ class PredictionProblem:
 
 
 def predict(p: PredictionProblem, with_variance: bool = False):
-    """Kriging mean Sigma_12 Sigma_22^-1 z (predict.py:65-87).  The
-    conditional-variance branch is not on the B200 path yet."""
-    if with_variance:
-        raise NotImplementedError("conditional variance is not on the B200 path (SURVEY 8(f) f3)")
+    """Kriging mean Sigma_12 Sigma_22^-1 z (predict.py:65-87); with_variance
+    (dense mode only, like the reference) also returns the conditional
+    covariance Sigma_11 - Sigma_12 Sigma_22^-1 Sigma_21, with Sigma_22^-1
+    applied by device solves on the factor of the same call."""
+    if with_variance and p.mode != "dense":
+        raise ValueError("conditional variance is available in dense mode only")
     coords = _coords_of(p.known)
     n = len(p.known)
     nb = min(p.tile_size(), n)
     h = _handle_for(coords, nb, p.max_rank, 1)
-    return h.predict(np.asarray(p.z, dtype=float), _coords_of(p.unknown), p.theta,
+    uxy = _coords_of(p.unknown)
+    pred = h.predict(np.asarray(p.z, dtype=float), uxy, p.theta,
                      p.accuracy if p.mode == "tlr" else None)
+    if not with_variance:
+        return pred
+    s12 = matern_block(uxy, coords, p.theta)           # m x n, device generated
+    s11 = matern_block(uxy, uxy, p.theta)
+    if p.theta.nugget:
+        s11[np.diag_indices_from(s11)] += p.theta.nugget
+    v = np.stack([h.solve(row) for row in s12], axis=1)   # Sigma_22^-1 Sigma_21 (n x m)
+    return pred, s11 - s12 @ v
 
 
 # ------------------------------------------------------ component entry points

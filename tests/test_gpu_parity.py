@@ -278,3 +278,16 @@ def test_distributed_path_world1(tb, gold):
         np.testing.assert_allclose(hd.apply_factor(x), hs.apply_factor(x), rtol=1e-12, atol=1e-12)
     hd.close()
     hs.close()
+
+
+def test_kriging_variance_device(tb):
+    """f3: conditional covariance (dense), predict.py:81-87 golden."""
+    g = np.load(GOLD / "variance.npz")
+    p = tb.MaternParams(1.0, 0.1, 0.5, 0.01)
+    pred, cov = tb.predict(tb.PredictionProblem(tb.LocationSet(g["known"]), g["z"], tb.LocationSet(g["unknown"]),
+                                                p, nb=100), with_variance=True)
+    np.testing.assert_allclose(pred, g["pred"], rtol=1e-9, atol=1e-11)
+    np.testing.assert_allclose(cov, g["cov"], rtol=1e-8, atol=1e-11)
+    with pytest.raises(ValueError):
+        tb.predict(tb.PredictionProblem(tb.LocationSet(g["known"]), g["z"], tb.LocationSet(g["unknown"]),
+                                        p, "tlr", 1e-9, 100), with_variance=True)
