@@ -55,9 +55,12 @@ struct tlrb_handle {
   double* dx = nullptr;
   double* dy = nullptr;
   double* diag = nullptr;
-  double* U = nullptr;
-  double* V = nullptr;
-  size_t slab = 0;               // doubles per U (or V) slab
+  // tile factors: rank-adaptive bump arena, reset at every factorisation;
+  // tile t owns U (nb x tcap[t]) and V (nb x tcap[t]), or a dense nb x nb
+  char* arena = nullptr;
+  size_t arena_bytes = 0, arena_off = 0, arena_peak = 0;
+  std::vector<double*> uptr, vptr;
+  std::vector<int> tcap;
   std::vector<int> rank;         // per lower tile
   std::vector<char> dense;       // per lower tile: stored dense (rank > max_rank), as L_ij^T in the U slab
   int* d_info = nullptr;         // [flag, tile, pivot]
@@ -105,8 +108,30 @@ struct tlrb_handle {
   size_t tid(int i, int j) const { return (size_t)i * (i - 1) / 2 + j; }
   bool dn(int i, int j) const { return dense[tid(i, j)] != 0; }
   bool live(int i, int j) const { return dense[tid(i, j)] || rank[tid(i, j)] > 0; }
-  double* Ut(int i, int j) const { return U + tid(i, j) * slab; }
-  double* Vt(int i, int j) const { return V + tid(i, j) * slab; }
+  double* Ut(int i, int j) const { return uptr[tid(i, j)]; }
+  double* Vt(int i, int j) const { return vptr[tid(i, j)]; }
+  void arena_reset() {
+    arena_off = 0;
+    std::fill(uptr.begin(), uptr.end(), nullptr);
+    std::fill(vptr.begin(), vptr.end(), nullptr);
+    std::fill(tcap.begin(), tcap.end(), 0);
+  }
+  double* arena_get(size_t doubles) {
+    const size_t a = (arena_off + 255) & ~(size_t)255;
+    if (a + doubles * sizeof(double) > arena_bytes)
+      throw CudaError(cudaErrorMemoryAllocation, "tile factor arena exhausted", __FILE__, __LINE__);
+    arena_off = a + doubles * sizeof(double);
+    arena_peak = std::max(arena_peak, arena_off);
+    return reinterpret_cast<double*>(arena + a);
+  }
+  // make tile t able to hold rank k (k == nb with dense: the whole L^T tile)
+  void ensure(size_t t, int k, bool dense_tile = false) {
+    if (k <= tcap[t] && (!dense_tile || tcap[t] >= nb)) return;
+    const int c = dense_tile ? nb : std::min(nb, (k + 15) & ~15);
+    uptr[t] = arena_get((size_t)nb * c);
+    vptr[t] = dense_tile ? nullptr : arena_get((size_t)nb * c);
+    tcap[t] = c;
+  }
   double* D(int i) const { return diag + (size_t)i * nb * nb; }
   void sync() {
     TLRB_CUDA(cudaStreamSynchronize(stream));
@@ -180,6 +205,8 @@ struct Job {
   bool factored = false;
   double* Qu = nullptr; double* Qv = nullptr; int mu = 0, nv = 0;
   double* Ufin = nullptr; double* Vfin = nullptr;
+  long tile = -1;     // destination tile (outputs allocated once the rank is known)
+  long ftile = -1;    // factored path: destination tile of Qu u_core / Qv v_core
 };
 
 void bind_slot(tlrb_handle* h, Job& J, int slot) {
@@ -289,12 +316,17 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     // one-sided Jacobi: per sweep s(s-1)/2 pairs x (3 dots + rotation) = 12 n flops each
     if (g_prof.on && J.s) g_prof.add_work(K_JACOBI, 6.0 * J.n * (double)J.s * (J.s - 1) * sw[j], 0);
     const int k = J.out_rank;
-    J.dense_out = h->max_rank > 0 && k > h->max_rank;
+    J.dense_out = h->max_rank > 0 && k > h->max_rank && !J.factored;
+    if (J.tile >= 0) {   // the destination tile's storage is sized by the new rank
+      if (J.dense_out || k) h->ensure((size_t)J.tile, J.dense_out ? h->nb : k, J.dense_out);
+      J.Uout = h->uptr[J.tile];
+      J.Vout = h->vptr[J.tile];
+      J.ldu = J.ldv = h->nb;
+    }
     if (J.dense_out) {   // A13: over the storage cap -> keep the tile exact (dense, transposed)
       cv.push_back({J.E, J.m, J.Uout, J.ldu, J.n, J.m, 1, 1.0, 0, nullptr});
       continue;
     }
-    if (k > h->cap) throw CudaError(cudaErrorMemoryAllocation, "tile rank exceeds slab capacity", __FILE__, __LINE__);
     if (!k) continue;
     cv.push_back({J.Vs, J.n, J.Vout, J.ldv, J.n, k, 0, 1.0, 0, d_perm + (size_t)j * h->nb});
     gu.push_back({J.E, J.Vout, nullptr, J.Uout, J.m, k, J.n, J.m, J.ldv, J.ldu, J.ldu, 0, 0, 0, 1.0, 0.0});
@@ -346,9 +378,7 @@ void compress_all(tlrb_handle* h, double acc) {
       const int off = i - j;
       J.s = off <= 2 ? J.n : std::min(J.n, 64);   // QRCP kernel hint (predicted steps)
       J.kind = 0;
-      J.Uout = h->Ut(i, j);
-      J.Vout = h->Vt(i, j);
-      J.ldu = J.ldv = h->nb;
+      J.tile = (long)h->tid(i, j);
       J.seed = h->tid(i, j) * 131 + 17;
       jobs.push_back(J);
       gen.push_back({J.M, J.m, h->off[i], J.m, h->off[j], J.n, 0.0});
@@ -398,9 +428,11 @@ void bcast_panel(tlrb_handle* h, int k, bool dense_mode) {
   for (int i = k + 1; i < h->t; ++i) {
     const int root = h->owner(i, k);
     if (dense_mode || h->dn(i, k)) {
+      h->ensure(h->tid(i, k), h->nb, true);
       bcast(h, h->Ut(i, k), (size_t)h->nb * h->sz[i], root);
     } else {
       const size_t r = h->rank[h->tid(i, k)];
+      if (r) h->ensure(h->tid(i, k), (int)r);
       bcast(h, h->Ut(i, k), (size_t)h->nb * r, root);
       bcast(h, h->Vt(i, k), (size_t)h->nb * r, root);
     }
@@ -632,8 +664,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           J.ldu = J.ldv = K;
           J.factored = true;
           J.Qu = Qu; J.Qv = Qv; J.mu = mi; J.nv = mj;
-          J.Ufin = h->Ut(i, j);
-          J.Vfin = h->Vt(i, j);
+          J.ftile = (long)h->tid(i, j);
           J.seed = 0;
           jobs.push_back(J);
           continue;
@@ -642,9 +673,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         J.n = mj;
         J.kind = 2;
         J.s = dij ? mj : sketch_guess(std::max(kij, di || dj ? mj : kj), mj);
-        J.Uout = h->Ut(i, j);
-        J.Vout = h->Vt(i, j);
-        J.ldu = J.ldv = nb;
+        J.tile = (long)h->tid(i, j);
         J.seed = (uint64_t)h->tid(i, j) * 7777 + (uint64_t)k * 131 + 5;
         double* X = J.E;
         double* Y = J.Y;
@@ -702,9 +731,12 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       compress_jobs(h, jobs, acc);
       {   // U_new = Qu u_core, V_new = Qv v_core (compression.py:81)
         std::vector<GemmProb> fu;
-        for (const Job& J : jobs) {
+        for (Job& J : jobs) {
           if (!J.factored || !J.out_rank) continue;
           const int kk = J.out_rank;
+          h->ensure((size_t)J.ftile, kk);
+          J.Ufin = h->uptr[J.ftile];
+          J.Vfin = h->vptr[J.ftile];
           fu.push_back({J.Qu, J.Uout, nullptr, J.Ufin, J.mu, kk, J.m, J.mu, J.ldu, nb, nb, 0, 0, 0, 1.0, 0.0});
           fu.push_back({J.Qv, J.Vout, nullptr, J.Vfin, J.nv, kk, J.n, J.nv, J.ldv, nb, nb, 0, 0, 0, 1.0, 0.0});
         }
@@ -933,6 +965,12 @@ int factorize(tlrb_handle* h, double th1, double th2, double th3, double nugget,
   TLRB_CUDA(cudaMemsetAsync(h->d_logdiag, 0, h->n * sizeof(double), s));
   TLRB_CUDA(cudaEventRecord(h->ev[0], s));
   const bool dense = acc == 0.0;
+  h->sync();   // previous users of the arena are done before it is recycled
+  h->arena_reset();
+  if (dense)
+    for (int i = 1; i < h->t; ++i)
+      for (int j = 0; j < i; ++j)
+        if (h->own(i, j)) h->ensure(h->tid(i, j), h->nb, true);
   generate(h, nugget, dense);
   TLRB_CUDA(cudaEventRecord(h->ev[1], s));
   std::fill(h->rank.begin(), h->rank.end(), 0);
@@ -1050,7 +1088,6 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     h->nb = (int)std::min<int64_t>(nb, n);
     h->t = (int)((n + h->nb - 1) / h->nb);
     h->max_rank = max_rank;
-    h->cap = h->nb;  // TLR slabs hold up to nb columns (max_rank only reported)
     for (int i = 0; i < h->t; ++i) {
       h->off.push_back(i * h->nb);
       h->sz.push_back((int)std::min<int64_t>(h->nb, n - (int64_t)i * h->nb));
@@ -1063,10 +1100,10 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMemcpy(h->dy, ys.data(), n * sizeof(double), cudaMemcpyHostToDevice));
     const size_t nb2 = (size_t)h->nb * h->nb;
     const size_t ntile = (size_t)h->t * (h->t - 1) / 2;
-    h->slab = (size_t)h->nb * h->cap;
     TLRB_CUDA(cudaMalloc(&h->diag, std::max<size_t>(1, h->t * nb2) * sizeof(double)));
-    TLRB_CUDA(cudaMalloc(&h->U, std::max<size_t>(1, ntile * h->slab) * sizeof(double)));
-    TLRB_CUDA(cudaMalloc(&h->V, std::max<size_t>(1, ntile * h->slab) * sizeof(double)));
+    h->uptr.assign(ntile, nullptr);
+    h->vptr.assign(ntile, nullptr);
+    h->tcap.assign(ntile, 0);
     h->rank.assign(ntile, 0);
     h->dense.assign(ntile, 0);
     TLRB_CUDA(cudaMalloc(&h->d_info, 4 * sizeof(int)));
@@ -1092,6 +1129,14 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMalloc(&h->d_rank, (size_t)h->max_jobs * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_sweeps, (size_t)h->max_jobs * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_perm, (size_t)h->max_jobs * h->nb * sizeof(int)));
+    {
+      size_t fb = 0, tb = 0;
+      TLRB_CUDA(cudaMemGetInfo(&fb, &tb));
+      const size_t full = std::max<size_t>(1, ntile) * 2 * nb2 * sizeof(double) + (1 << 20);
+      const size_t avail = (size_t)(0.85 * (double)fb);
+      h->arena_bytes = std::min(full, avail);
+      TLRB_CUDA(cudaMalloc(&h->arena, h->arena_bytes));
+    }
     return TLRB_OK;
   });
   if (rc != TLRB_OK) {
@@ -1149,7 +1194,7 @@ void tlrb_destroy(tlrb_handle* h) {
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->d_ibuf) cudaFree(h->d_ibuf);
   if (h->d_acc) cudaFree(h->d_acc);
-  void* ptrs[] = {h->dx, h->dy, h->diag, h->U, h->V, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
+  void* ptrs[] = {h->dx, h->dy, h->diag, h->arena, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
                   h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_y, h->d_ux, h->d_uy,
                   h->d_pred, h->d_partial};
   for (void* p : ptrs)
