@@ -291,3 +291,23 @@ def test_kriging_variance_device(tb):
     with pytest.raises(ValueError):
         tb.predict(tb.PredictionProblem(tb.LocationSet(g["known"]), g["z"], tb.LocationSet(g["unknown"]),
                                         p, "tlr", 1e-9, 100), with_variance=True)
+
+
+def test_c3_full_dense_parity(tb):
+    """Full C3 (n = 62,500, nb = 760): dense log-likelihood vs the reference's
+    value on the reference's own z (tests/golden/make_c3_golden.py, ~25 min
+    of CPU).  The C3 TLR reference (~5 h) is not generated."""
+    import json
+    p = GOLD / "c3.json"
+    if not p.exists():
+        pytest.skip("C3 golden not generated")
+    e = json.loads(p.read_text())["C3"]
+    locs = tb.generate_locations(e["n"], 0)
+    z = np.load(GOLD / "z_c3.npz")["C3"]
+    ll = tb.log_likelihood(locs, z, tb.MaternParams(*e["theta"]), tb.LikelihoodConfig(nb=e["nb"]))
+    ref = e["modes"]["dense"]["ll"]
+    assert abs(ll - ref) <= 1e-10 * abs(ref), (ll, ref)
+    # TLR(1e-7) with the C3 storage cap stays within the C3p-measured TLR gap of dense
+    llt = tb.log_likelihood(locs, z, tb.MaternParams(*e["theta"]),
+                            tb.LikelihoodConfig(mode="tlr", accuracy=1e-7, nb=e["nb"], max_rank=380))
+    assert abs(llt - ref) <= 10 * 1e-7 * abs(ref)
