@@ -21,6 +21,8 @@ namespace cg = cooperative_groups;
 
 namespace tlrb {
 
+__device__ long long* g_qrcp_prof = nullptr;   // optional phase counters (debug)
+
 __device__ __forceinline__ double A_ld(const double* a, size_t i) { return __ldcg(a + i); }
 
 __device__ __forceinline__ double wsum_q(double v) {
@@ -294,6 +296,9 @@ __global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __rest
       pend = -1;
     }
   };
+  long long c_cand = 0, c_fetch = 0, c_refl = 0, c_upd = 0, c_pub = 0, c_sync = 0;
+  long long tt = clock64();
+  auto tick = [&](long long& a) { const long long nw_ = clock64(); a += nw_ - tt; tt = nw_; };
   for (; j < kmax; ++j) {
     const int par = j & 1;
     if (warp == 0) {
@@ -322,6 +327,7 @@ __global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __rest
     // the barrier, so nobody reads it any more); v is still that reflector
     flush_pending();
     resid = s_resid;
+    tick(c_cand);
     if (s_stop) break;
     const int p = s_piv;
     const int owner = p / cpc;
@@ -337,6 +343,7 @@ __global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __rest
     part = wsum_q(part);
     if (lane == 0) red[warp] = part;
     __syncthreads();
+    tick(c_fetch);
     if (warp == 0) {
       double ss = lane < nw ? red[lane] : 0.0;
       ss = wsum_q(ss);
@@ -364,6 +371,7 @@ __global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __rest
       if (tid == 0) done[pend] = 1;
     }
     __syncthreads();
+    tick(c_refl);
     for (int k = warp; k < nloc; k += nw) {
       if (done[k]) continue;
       double* col = Ac + (size_t)k * m;
@@ -391,8 +399,15 @@ __global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __rest
       if (lane == 0) cn[k] = a;
     }
     __syncthreads();
+    tick(c_upd);
     publish(par ^ 1);
+    tick(c_pub);
     cl.sync();
+    tick(c_sync);
+  }
+  if (g_qrcp_prof && blockIdx.x < 16 && tid == 0) {
+    long long* q = g_qrcp_prof + 8 * blockIdx.x;
+    q[0] = c_cand; q[1] = c_fetch; q[2] = c_refl; q[3] = c_upd; q[4] = c_pub; q[5] = c_sync; q[6] = j;
   }
   flush_pending();
   // write the slab back; remaining columns go to perm[j..n) in index order
@@ -445,10 +460,21 @@ static int cluster_cpc(int mmax, int nmax, int& CL) {
   cpc = std::min(cpc, 64);
   CL = (nmax + cpc - 1) / cpc;
   if (cpc < 8 || CL > 16 || mmax > 1024) return 0;
+  // spread over the full 16-CTA cluster: one column per warp per pivot step
+  // (the per-step column update is the longest phase)
+  CL = std::max(CL, std::min(16, (nmax + 31) / 32));
   return (nmax + CL - 1) / CL;
 }
 
 static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
+  static long long* d_prof = nullptr;
+  if (getenv("TLRB_QRCP_PROF")) {
+    if (!d_prof) {
+      TLRB_CUDA(cudaMalloc(&d_prof, 16 * 8 * sizeof(long long)));
+      TLRB_CUDA(cudaMemcpyToSymbol(g_qrcp_prof, &d_prof, sizeof d_prof));
+    }
+    TLRB_CUDA(cudaMemsetAsync(d_prof, 0, 16 * 8 * sizeof(long long), s));
+  }
   int CL = 0;
   const int cpc = cluster_cpc(L.mmax, L.nmax, CL);
   const size_t smem = ((size_t)cpc * L.mmax + (size_t)L.mmax + cpc) * 8;
@@ -470,6 +496,15 @@ static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
   cfg.numAttrs = 1;
   TLRB_CUDA(cudaLaunchKernelEx(&cfg, kern, L.dp, cpc));
   post_launch();
+  if (d_prof && getenv("TLRB_QRCP_PROF")) {
+    long long hp[16 * 8];
+    TLRB_CUDA(cudaMemcpyAsync(hp, d_prof, sizeof hp, cudaMemcpyDeviceToHost, s));
+    TLRB_CUDA(cudaStreamSynchronize(s));
+    for (int c = 0; c < 16; ++c)
+      if (hp[8 * c + 6])
+        fprintf(stderr, "[qrcp-prof] cta %d cand %lld fetch %lld refl %lld upd %lld pub %lld sync %lld steps %lld\n", c,
+                hp[8 * c], hp[8 * c + 1], hp[8 * c + 2], hp[8 * c + 3], hp[8 * c + 4], hp[8 * c + 5], hp[8 * c + 6]);
+  }
 }
 
 static void run_single(const QrcpLaunch& L, cudaStream_t s) {
