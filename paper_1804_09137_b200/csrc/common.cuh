@@ -33,7 +33,7 @@ inline void post_launch() {
 }
 
 // ---- per-kernel-class profiler (CUDA events on the launching stream) ----
-enum KClass { K_GEN = 0, K_GEMM, K_TRSM, K_POTRF, K_QR, K_JACOBI, K_SUMSQ, K_COPY, K_GAUSS,
+enum KClass { K_GEN = 0, K_GEMM, K_TRSM, K_POTRF, K_QR, K_JACOBI, K_SUMSQ, K_COPY, K_UNUSED,
               K_REDUCE, K_CROSS, K_NCLASS };
 extern const char* kclass_name[K_NCLASS];
 struct Profiler {
@@ -123,7 +123,6 @@ struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; in
                   int tri; const int* rowperm; const int* srccol = nullptr; };
 struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid_out; double stop_rel2;
                   int hint = 0; };   // hint: predicted number of QRCP steps (selects the kernel)
-struct GaussProb { double* A; int ld, m, n; uint64_t seed; };
 
 // Device-resident descriptor staging (pinned host ring -> device), reset at
 // stream synchronisation points.
@@ -156,7 +155,6 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);
-void launch_gaussian(const std::vector<GaussProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sum_log(const double* logdiag, int n, double* out, cudaStream_t s);
 void launch_dot(const double* x, int n, double* out, cudaStream_t s);
 void launch_cross_gemv(const double* kx, const double* ky, const double* w, int64_t n,

@@ -393,6 +393,15 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     g = std::min(g, max_g);
     groups[g].push_back(p);
   }
+  // throughput mode: when a group would need far more CTAs than the GPU has
+  // SMs, halve its cluster size (large clusters co-schedule poorly and pay
+  // more barrier waits); in latency mode (few matrices) keep the wide clusters
+  static const int budget = getenv("TLRB_JACOBI_CTA_BUDGET") ? atoi(getenv("TLRB_JACOBI_CTA_BUDGET")) : (1 << 30);   // measured: wide clusters win
+  for (int g = 4; g >= 2; --g)
+    if ((int)groups[g].size() * (1 << g) > budget) {
+      for (const JacobiProb& p : groups[g]) groups[g - 1].push_back(p);
+      groups[g].clear();
+    }
   // independent problem groups run concurrently: the largest-cluster group
   // on the caller's stream, the others on side streams forked/joined with
   // events (they would otherwise serialise behind each other)

@@ -9,7 +9,7 @@ namespace tlrb {
 int64_t g_launches = 0;
 Profiler g_prof;
 const char* kclass_name[K_NCLASS] = {"gen_tiles", "dgemm_vbatch", "trsm_vbatch", "potrf_block",
-                                     "qr_householder", "jacobi_svd", "sumsq", "copy", "gaussian",
+                                     "qr_householder", "jacobi_svd", "sumsq", "copy", "unused",
                                      "reduce", "cross_gemv"};
 
 cudaEvent_t Profiler::get() {
@@ -143,39 +143,6 @@ void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t
   for (const CopyProb& p : keep) by += 16.0 * p.m * p.n;
   ProfScope ps(K_COPY, s, 0, by);
   copy_kernel<<<(unsigned)(keep.size() * chunks), 256, 0, s>>>(dp, chunks);
-  post_launch();
-}
-
-// ------------------------------------------------------- Gaussian sketch
-__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
-  z += 0x9e3779b97f4a7c15ull;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
-}
-
-__global__ void __launch_bounds__(256) gaussian_kernel(const GaussProb* __restrict__ probs) {
-  const GaussProb P = probs[blockIdx.y];
-  const int64_t tot = (int64_t)P.m * P.n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e % P.m), c = (int)(e / P.m);
-    const uint64_t h1 = splitmix(P.seed ^ (uint64_t)e * 0x2545F4914F6CDD1Dull);
-    const uint64_t h2 = splitmix(h1);
-    const double u1 = ((h1 >> 11) + 1) * (1.0 / 9007199254740993.0);   // (0,1]
-    const double u2 = (h2 >> 11) * (1.0 / 9007199254740992.0);         // [0,1)
-    P.A[(size_t)c * P.ld + r] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
-  }
-}
-
-void launch_gaussian(const std::vector<GaussProb>& probs, DescArena& ar, cudaStream_t s) {
-  if (probs.empty()) return;
-  const GaussProb* dp = ar.put(probs, s);
-  double by = 0;
-  for (const GaussProb& p : probs) by += 8.0 * p.m * p.n;
-  ProfScope ps(K_GAUSS, s, 0, by);
-  dim3 grid(16, (unsigned)probs.size());
-  gaussian_kernel<<<grid, 256, 0, s>>>(dp);
   post_launch();
 }
 

@@ -34,8 +34,8 @@ using namespace tlrb;
 
 namespace {
 
-constexpr double kSketchRelTol = 1e-3;   // sketch residual <= 1e-3 * acc * ||M||_F
-constexpr double kFullSketchFrac = 0.7;  // sketches this wide fall back to the full tile
+// truncated QRCP stops at ||residual||_F <= 1e-3 acc ||M||_F
+constexpr double kQrcpRelTol = 1e-3;
 constexpr int kPotrfBlock = 32;
 
 struct Flops {
@@ -192,14 +192,14 @@ __global__ void axpy_kernel(double* y, const double* x, double a, int n) {
 // ------------------------------------------------------------ compression
 struct Job {
   int m, n;           // M is m x n
-  int s;              // sketch width (== n: unsketched)
+  int s;              // QRCP kernel hint on entry; QRCP rank r (Jacobi width) after it
   int kind;           // bit1: recompression (noise floor)
   double* M;          // slot pointers
   double* E; double* Y; double* Q; double* Om; double* Bt; double* Vs; double* sig; double* T;
   double* Uout; double* Vout; int ldu, ldv;
   int out_rank;
   bool dense_out;     // rank above max_rank: stored dense (L^T in Uout, ld ldu)
-  uint64_t seed;
+  uint64_t seed;      // unused (kept for descriptor stability)
   // factored recompression (compression.py:54-81): M is the K x K core,
   // U_new = Qu u_core, V_new = Qv v_core are formed after compress_jobs
   bool factored = false;
@@ -244,7 +244,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
       Job& J = jobs[j];
       cp.push_back({J.M, J.m, J.E, J.m, J.m, J.n, 0, 1.0, 0, nullptr});
       qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, h->d_rank + j, h->d_sums + 6 * j + 1,
-                    (kSketchRelTol * acc) * (kSketchRelTol * acc), J.s});
+                    (kQrcpRelTol * acc) * (kQrcpRelTol * acc), J.s});
     }
     launch_copy(cp, h->ar, s);
     launch_qrcp(qp, gathered, h->ar, s);
@@ -335,7 +335,8 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   launch_gemm(gu, h->ar, s);
 }
 
-int sketch_guess(int prev_rank, int n) {
+// predicted number of QRCP steps of an update (selects the QRCP kernel)
+int rank_hint(int prev_rank, int n) {
   int s = (int)std::ceil(1.25 * prev_rank) + 32;
   s = (s + 7) & ~7;
   return std::min(s, n);
@@ -672,7 +673,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         J.m = mi;
         J.n = mj;
         J.kind = 2;
-        J.s = dij ? mj : sketch_guess(std::max(kij, di || dj ? mj : kj), mj);
+        J.s = dij ? mj : rank_hint(std::max(kij, di || dj ? mj : kj), mj);
         J.tile = (long)h->tid(i, j);
         J.seed = (uint64_t)h->tid(i, j) * 7777 + (uint64_t)k * 131 + 5;
         double* X = J.E;
