@@ -12,7 +12,9 @@
  *   linalg.solve_cholesky       linalg.py:195-197  -> tlrb_solve
  *   predict.predict (mean)      predict.py:65-87   -> tlrb_predict
  *   kernels.bessel_k            kernels.py:216-226 -> tlrb_bessel_k
- *   kernels.matern_block        kernels.py:494-530 -> tlrb_matern_block
+ *   kernels.matern_block        kernels.py:494-530 -> tlrb_matern_block(_metric)
+ *   geometry.GreatCircle / LocationSet(..., GreatCircle(r)) geometry.py:24-31,80-122
+ *                               kernels.py:460-491 -> tlrb_set_metric
  *   compression.compress_tile   compression.py:39-51 -> tlrb_compress_tile
  *   linalg.NotPositiveDefiniteError linalg.py:20-33 -> TLRB_ERR_NPD + tlrb_last_error
  *
@@ -75,6 +77,13 @@ tlrb_handle* tlrb_create_dist(const double* xy, int64_t n, int32_t nb, int32_t m
                               int32_t device, int32_t rank, int32_t world, int32_t P,
                               int32_t Q, const char* nccl_id, int32_t* err);
 
+/* Distance metric of the handle's locations.  sphere_radius == 0: Euclidean
+ * (the default after create); > 0: great-circle (haversine) distance on a
+ * sphere of that radius, xy read as (lon, lat) in degrees with |lon| <= 180,
+ * |lat| <= 90 (else TLRB_ERR_ARG) — geometry.GreatCircle.  Applies to every
+ * later evaluation, including the unknown points of tlrb_predict. */
+int32_t tlrb_set_metric(tlrb_handle* h, double sphere_radius);
+
 /* One Gaussian log-likelihood evaluation
  *   ll = -0.5 (n log 2pi + log|Sigma| + z' Sigma^-1 z)     (stats.py:112)
  * z: host pointer (n doubles).  acc == 0 -> dense mode, else TLR(acc).
@@ -128,6 +137,10 @@ int32_t tlrb_bessel_k(double nu, const double* x, int64_t count, double* out,
 int32_t tlrb_matern_block(const double* rows_xy, int64_t m, const double* cols_xy,
                           int64_t n, double theta1, double theta2, double theta3,
                           double* out, int32_t device);
+/* Same with a metric: sphere_radius as in tlrb_set_metric (kernels.py:460-491). */
+int32_t tlrb_matern_block_metric(const double* rows_xy, int64_t m, const double* cols_xy,
+                                 int64_t n, double theta1, double theta2, double theta3,
+                                 double sphere_radius, double* out, int32_t device);
 
 /* Compress one dense m x n tile (column-major) to relative Frobenius accuracy
  * acc with the device compressor (compression.py:39-51).  u: m x k, v: n x k

@@ -186,12 +186,27 @@ def matern_t(t, theta1: float, nu: float) -> np.ndarray:
     return out
 
 
-def matern_block(rows_xy: np.ndarray, cols_xy: np.ndarray, theta) -> np.ndarray:
-    """Dense Euclidean kernel block, no nugget.  kernels.py:436-443 / 494-530."""
+def distance_block(rows_xy: np.ndarray, cols_xy: np.ndarray, radius: float = 0.0) -> np.ndarray:
+    """Pairwise distances.  radius == 0: Euclidean (kernels.py:436-443);
+    radius > 0: haversine on (lon, lat) degrees through the KernelView
+    (lat, lon radians, cos lat; geometry.py:106-122) in the operation order
+    of kernels.py:461-473."""
+    if radius == 0.0:
+        dx = rows_xy[:, 0:1] - cols_xy[None, :, 0]
+        dy = rows_xy[:, 1:2] - cols_xy[None, :, 1]
+        return np.sqrt(dx * dx + dy * dy)
+    plat, plon = np.radians(rows_xy[:, 1])[:, None], np.radians(rows_xy[:, 0])[:, None]
+    qlat, qlon = np.radians(cols_xy[:, 1])[None, :], np.radians(cols_xy[:, 0])[None, :]
+    sp = np.sin(0.5 * (qlat - plat))
+    sl = np.sin(0.5 * (qlon - plon))
+    a = np.minimum(sp * sp + np.cos(plat) * np.cos(qlat) * sl * sl, 1.0)
+    return (2.0 * radius) * np.arcsin(np.sqrt(a))
+
+
+def matern_block(rows_xy: np.ndarray, cols_xy: np.ndarray, theta, radius: float = 0.0) -> np.ndarray:
+    """Dense kernel block, no nugget.  kernels.py:436-491 / 494-530."""
     th1, th2, nu = theta[0], theta[1], theta[2]
-    dx = rows_xy[:, 0:1] - cols_xy[None, :, 0]
-    dy = rows_xy[:, 1:2] - cols_xy[None, :, 1]
-    t = np.sqrt(dx * dx + dy * dy) * (1.0 / th2)
+    t = distance_block(rows_xy, cols_xy, radius) * (1.0 / th2)
     return matern_t(t, th1, nu)
 
 
@@ -239,7 +254,7 @@ def recompress(u1, v1, u2, v2, eps: float):
     return qu @ (w[:, :k] * s[:k]), qv @ zt[:k].T
 
 
-def assemble(xy: np.ndarray, theta, nb: int, acc: float | None):
+def assemble(xy: np.ndarray, theta, nb: int, acc: float | None, radius: float = 0.0):
     """Lower-triangle tile assembly; TLR mode compresses each off-diagonal tile.
     tilestore.py:181-223.  Returns (diag list, lower dict)."""
     n = xy.shape[0]
@@ -247,13 +262,13 @@ def assemble(xy: np.ndarray, theta, nb: int, acc: float | None):
     nugget = theta[3] if len(theta) > 3 else 0.0
     diag, lower = [], {}
     for i, (r0, r1) in enumerate(bnds):
-        d = matern_block(xy[r0:r1], xy[r0:r1], theta)
+        d = matern_block(xy[r0:r1], xy[r0:r1], theta, radius)
         if nugget:
             d[np.diag_indices_from(d)] += nugget
         diag.append(d)
         for j in range(i):
             c0, c1 = bnds[j]
-            blk = matern_block(xy[r0:r1], xy[c0:c1], theta)
+            blk = matern_block(xy[r0:r1], xy[c0:c1], theta, radius)
             lower[(i, j)] = compress_tile(blk, acc) if acc else blk
     return diag, lower
 
@@ -345,23 +360,23 @@ def backward_solve(D, L, n, nb, rhs):
     return x
 
 
-def log_likelihood(xy, z, theta, nb, acc=None):
+def log_likelihood(xy, z, theta, nb, acc=None, radius=0.0):
     """-0.5 (n log 2pi + log|Sigma| + z' Sigma^-1 z).  stats.py:96-112.
     Returns (ll, log_det, quad)."""
     n = xy.shape[0]
     nb = min(nb, n)
-    D, L, log_det = cholesky(*assemble(xy, theta, nb, acc), acc)
+    D, L, log_det = cholesky(*assemble(xy, theta, nb, acc, radius), acc)
     y = forward_solve(D, L, n, nb, z)
     quad = float(y @ y)
     return -0.5 * (n * LOG_2PI + log_det + quad), log_det, quad
 
 
-def sample_measurements(xy, theta, seed: int) -> np.ndarray:
+def sample_measurements(xy, theta, seed: int, radius: float = 0.0) -> np.ndarray:
     """z = L w, dense nb=min(200,n), w ~ N(0,1) from default_rng(seed).
     stats.py:115-133."""
     n = xy.shape[0]
     nb = min(200, n)
-    D, L, _ = cholesky(*assemble(xy, theta, nb, None), None)
+    D, L, _ = cholesky(*assemble(xy, theta, nb, None, radius), None)
     w = np.random.default_rng(seed).standard_normal(n)
     b = tile_bounds(n, nb)
     out = np.zeros(n)
@@ -372,13 +387,13 @@ def sample_measurements(xy, theta, seed: int) -> np.ndarray:
     return out
 
 
-def predict(known_xy, z, unknown_xy, theta, nb, acc=None):
+def predict(known_xy, z, unknown_xy, theta, nb, acc=None, radius=0.0):
     """Kriging mean S12 S22^-1 z.  predict.py:65-87 (mean branch)."""
     n = known_xy.shape[0]
     nb = min(nb, n)
-    D, L, _ = cholesky(*assemble(known_xy, theta, nb, acc), acc)
+    D, L, _ = cholesky(*assemble(known_xy, theta, nb, acc, radius), acc)
     w = backward_solve(D, L, n, nb, forward_solve(D, L, n, nb, z))
-    return matern_block(unknown_xy, known_xy, theta) @ w
+    return matern_block(unknown_xy, known_xy, theta, radius) @ w
 
 
 # --------------------------------------------------------------------------

@@ -1,7 +1,10 @@
 """B200-native TLR Gaussian log-likelihood (drop-in for tlrgeo's likelihood
 and kriging path).  All numerics run in libtlrb200.so (sm_100a CUDA)."""
 from .api import (  # noqa: F401
+    EARTH_RADIUS_KM,
     DeviceError,
+    Euclidean,
+    GreatCircle,
     Handle,
     LikelihoodConfig,
     LocationSet,
@@ -18,10 +21,18 @@ from .api import (  # noqa: F401
     predict,
     sample_measurements,
 )
+from .dataio import (  # noqa: F401
+    DataError,
+    Dataset,
+    load_dataset,
+    partition_regions,
+    save_dataset,
+)
 
 __all__ = [
-    "DeviceError", "Handle", "LikelihoodConfig", "LocationSet", "MaternParams",
+    "EARTH_RADIUS_KM", "DeviceError", "Euclidean", "GreatCircle", "Handle", "LikelihoodConfig", "LocationSet", "MaternParams",
     "NotPositiveDefiniteError", "PredictionProblem", "bessel_k", "compress_tile",
     "generate_locations", "launch_count", "log_likelihood", "log_likelihood_parts",
     "matern_block", "predict", "sample_measurements",
+    "DataError", "Dataset", "load_dataset", "partition_regions", "save_dataset",
 ]

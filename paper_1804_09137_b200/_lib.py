@@ -50,6 +50,7 @@ SIGNATURES = [
     ("tlrb_nccl_unique_id", C.c_int32, [C.c_char_p, C.c_int32]),
     ("tlrb_create_dist", C.c_void_p, [_DP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.c_int32, C.c_char_p, _IP]),
+    ("tlrb_set_metric", C.c_int32, [C.c_void_p, C.c_double]),
     ("tlrb_loglik", C.c_int32, [C.c_void_p, _DP, C.c_double, C.c_double, C.c_double, C.c_double,
                                 C.c_double, _DP, _DP, _DP, C.POINTER(TlrbStats)]),
     ("tlrb_loglik_device", C.c_int32, [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
@@ -65,6 +66,8 @@ SIGNATURES = [
     ("tlrb_bessel_k", C.c_int32, [C.c_double, _DP, C.c_int64, _DP, C.c_int32]),
     ("tlrb_matern_block", C.c_int32, [_DP, C.c_int64, _DP, C.c_int64, C.c_double, C.c_double,
                                       C.c_double, _DP, C.c_int32]),
+    ("tlrb_matern_block_metric", C.c_int32, [_DP, C.c_int64, _DP, C.c_int64, C.c_double, C.c_double,
+                                             C.c_double, C.c_double, _DP, C.c_int32]),
     ("tlrb_compress_tile", C.c_int32, [_DP, C.c_int32, C.c_int32, C.c_double, _IP, _DP, _DP, C.c_int32]),
     ("tlrb_launch_count", C.c_int64, []),
     ("tlrb_profile_enable", C.c_int32, [C.c_int32]),

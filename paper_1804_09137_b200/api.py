@@ -4,7 +4,8 @@ Mirrors (names, argument meaning, error behaviour) the reference package
 `tlrgeo` (/root/reference/pkg/src/tlrgeo):
 
   MaternParams          kernels.py:34-65
-  LocationSet           geometry.py:78-149 (Euclidean metric)
+  Euclidean, GreatCircle geometry.py:16-33
+  LocationSet           geometry.py:78-149 (both metrics)
   generate_locations    geometry.py:186-206
   LikelihoodConfig      stats.py:41-70   (+ max_rank, ngpus)
   log_likelihood        stats.py:103-112
@@ -77,17 +78,53 @@ class MaternParams:
         return (self.theta1, self.theta2, self.theta3, self.nugget)
 
 
+EARTH_RADIUS_KM = 6371.0       # geometry.py:16
+
+
+@dataclass(frozen=True)
+class Euclidean:
+    """Planar distance (geometry.py:19-21)."""
+
+
+@dataclass(frozen=True)
+class GreatCircle:
+    """Haversine distance on a sphere of `radius`; coordinates are
+    (lon, lat) in degrees (geometry.py:24-31)."""
+
+    radius: float = EARTH_RADIUS_KM
+
+    def __post_init__(self):
+        if not (self.radius > 0) or not math.isfinite(self.radius):
+            raise ValueError(f"sphere radius must be positive, got {self.radius}")
+
+
+def sphere_radius(metric) -> float:
+    """0.0 for Euclidean, the sphere radius for great circle.  Accepts this
+    module's metrics and the reference's (matched by class name)."""
+    name = type(metric).__name__
+    if metric is None or name == "Euclidean":
+        return 0.0
+    if name == "GreatCircle":
+        return float(metric.radius)
+    raise ValueError(f"unsupported metric {metric!r}")
+
+
 class LocationSet:
-    """Ordered set of distinct unit-square (Euclidean) locations, (n, 2)."""
+    """Ordered set of distinct locations, (n, 2), with a metric
+    (geometry.py:78-97: same validation and errors)."""
 
     def __init__(self, coords, metric=None):
+        metric = Euclidean() if metric is None else metric
         coords = np.ascontiguousarray(coords, dtype=float)
         if coords.ndim != 2 or coords.shape[1] != 2 or coords.shape[0] == 0:
             raise ValueError(f"coords must be a non-empty (n, 2) array, got {coords.shape}")
         if not np.isfinite(coords).all():
             raise ValueError("locations must be finite")
-        if metric is not None and type(metric).__name__ != "Euclidean":
-            raise ValueError("only the Euclidean metric is on the B200 path")
+        if sphere_radius(metric) > 0:
+            lon, lat = coords[:, 0], coords[:, 1]
+            if (np.abs(lon) > 180).any() or (np.abs(lat) > 90).any():
+                raise ValueError("great-circle coordinates must satisfy "
+                                 "lon in [-180, 180], lat in [-90, 90]")
         if np.unique(coords, axis=0).shape[0] != coords.shape[0]:
             raise ValueError("locations must be pairwise distinct")
         coords.setflags(write=False)
@@ -149,9 +186,10 @@ class Handle:
     arenas reused across evaluations (one MLE run = one handle)."""
 
     def __init__(self, coords: np.ndarray, nb: int, max_rank: int = 0, ngpus: int = 1,
-                 device: int = 0, dist: tuple | None = None):
+                 device: int = 0, dist: tuple | None = None, radius: float = 0.0):
         """dist = (rank, world, P, Q, nccl_id_bytes): 2D block-cyclic multi-GPU
-        handle (one process per GPU); see `distributed_handle`."""
+        handle (one process per GPU); see `distributed_handle`.  radius > 0:
+        great-circle metric on that sphere, coords = (lon, lat) degrees."""
         self.lib = _lib.load()
         xy = np.ascontiguousarray(coords, dtype=np.float64)
         self.n = xy.shape[0]
@@ -168,6 +206,11 @@ class Handle:
             raise (ValueError if err[0] == _lib.TLRB_ERR_ARG else DeviceError)(
                 f"tlrb_create failed (code {int(err[0])})")
         self.last_stats: dict | None = None
+        self.radius = float(radius)
+        if self.radius:
+            rc = self.lib.tlrb_set_metric(self.h, self.radius)
+            if rc:
+                self._raise(rc)
 
     def close(self):
         if getattr(self, "h", None):
@@ -263,7 +306,7 @@ def nccl_unique_id() -> bytes:
 
 
 def distributed_handle(coords, nb: int, max_rank: int = 0, P: int | None = None,
-                       Q: int | None = None, device: int | None = None) -> Handle:
+                       Q: int | None = None, device: int | None = None, radius: float = 0.0) -> Handle:
     """Handle over all ranks of the default torch.distributed group (one
     process per GPU): 2D block-cyclic tiles on a P x Q grid.
     Single process without torch.distributed: world = 1."""
@@ -284,22 +327,23 @@ def distributed_handle(coords, nb: int, max_rank: int = 0, P: int | None = None,
     if device is None:
         import os
         device = int(os.environ.get("LOCAL_RANK", "0"))
-    return Handle(coords, nb, max_rank, device=device, dist=(rank, world, P, Q, nid))
+    return Handle(coords, nb, max_rank, device=device, dist=(rank, world, P, Q, nid), radius=radius)
 
 
 _HANDLES: dict = {}
 
 
-def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus) -> Handle:
-    key = (coords.__array_interface__["data"][0], coords.shape[0], int(nb), int(max_rank or 0), ngpus)
+def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus, radius: float = 0.0) -> Handle:
+    key = (coords.__array_interface__["data"][0], coords.shape[0], int(nb), int(max_rank or 0), ngpus,
+           radius)
     h = _HANDLES.get(key)
     if h is None or h[0] is not coords:
         if len(_HANDLES) > 8:
             _HANDLES.clear()
         if ngpus and ngpus > 1:   # one process per GPU under torch.distributed
-            h = (coords, distributed_handle(coords, nb, max_rank or 0))
+            h = (coords, distributed_handle(coords, nb, max_rank or 0, radius=radius))
         else:
-            h = (coords, Handle(coords, nb, max_rank or 0))
+            h = (coords, Handle(coords, nb, max_rank or 0, radius=radius))
         _HANDLES[key] = h
     return h[1]
 
@@ -309,6 +353,10 @@ def _coords_of(locs) -> np.ndarray:
     if coords is None:
         raise TypeError("locs must be a LocationSet (with .coords)")
     return coords
+
+
+def _radius_of(locs) -> float:
+    return sphere_radius(getattr(locs, "metric", None))
 
 
 def log_likelihood(locs, z, p: MaternParams, cfg: LikelihoodConfig = LikelihoodConfig()) -> float:
@@ -322,7 +370,7 @@ def log_likelihood(locs, z, p: MaternParams, cfg: LikelihoodConfig = LikelihoodC
         raise ValueError(f"measurement vector shape {z.shape} does not match n={n}")
     coords = _coords_of(locs)
     nb = min(cfg.tile_size(), n)
-    h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus)
+    h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus, _radius_of(locs))
     acc = cfg.accuracy if cfg.mode == "tlr" else None
     ll, _, _ = h.loglik(z, p, acc)
     return ll
@@ -333,7 +381,7 @@ def log_likelihood_parts(locs, z, p: MaternParams, cfg: LikelihoodConfig = Likel
     z = np.asarray(z, dtype=float)
     coords = _coords_of(locs)
     nb = min(cfg.tile_size(), len(locs))
-    h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus)
+    h = _handle_for(coords, nb, cfg.max_rank, cfg.ngpus, _radius_of(locs))
     ll, ld, q = h.loglik(z, p, cfg.accuracy if cfg.mode == "tlr" else None)
     return ll, ld, q, h.last_stats
 
@@ -344,7 +392,7 @@ def sample_measurements(locs, p_true: MaternParams, seed: int) -> np.ndarray:
     standard normals (the reference's own stream, drawn on the host)."""
     coords = _coords_of(locs)
     n = coords.shape[0]
-    h = Handle(coords, min(DEFAULT_NB_DENSE, n))
+    h = Handle(coords, min(DEFAULT_NB_DENSE, n), radius=_radius_of(locs))
     try:
         h.factorize(p_true, None)
         w = np.random.default_rng(seed).standard_normal(n)
@@ -367,6 +415,9 @@ class PredictionProblem:
     max_rank: int | None = None
 
     def __post_init__(self):
+        mk, mu = getattr(self.known, "metric", None), getattr(self.unknown, "metric", None)
+        if sphere_radius(mk) != sphere_radius(mu):
+            raise ValueError("known and unknown sets use different metrics")
         z = np.asarray(self.z, dtype=float)
         if z.shape != (len(self.known),):
             raise ValueError(f"measurement shape {z.shape} does not match {len(self.known)} locations")
@@ -391,14 +442,15 @@ def predict(p: PredictionProblem, with_variance: bool = False):
     coords = _coords_of(p.known)
     n = len(p.known)
     nb = min(p.tile_size(), n)
-    h = _handle_for(coords, nb, p.max_rank, 1)
+    radius = _radius_of(p.known)
+    h = _handle_for(coords, nb, p.max_rank, 1, radius)
     uxy = _coords_of(p.unknown)
     pred = h.predict(np.asarray(p.z, dtype=float), uxy, p.theta,
                      p.accuracy if p.mode == "tlr" else None)
     if not with_variance:
         return pred
-    s12 = matern_block(uxy, coords, p.theta)           # m x n, device generated
-    s11 = matern_block(uxy, uxy, p.theta)
+    s12 = matern_block(uxy, coords, p.theta, radius)   # m x n, device generated
+    s11 = matern_block(uxy, uxy, p.theta, radius)
     if p.theta.nugget:
         s11[np.diag_indices_from(s11)] += p.theta.nugget
     v = np.stack([h.solve(row) for row in s12], axis=1)   # Sigma_22^-1 Sigma_21 (n x m)
@@ -417,14 +469,15 @@ def bessel_k(nu: float, x) -> np.ndarray:
     return out
 
 
-def matern_block(rows_xy, cols_xy, p: MaternParams) -> np.ndarray:
-    """Dense kernel block on the device (kernels.py:494-530, no nugget)."""
+def matern_block(rows_xy, cols_xy, p: MaternParams, radius: float = 0.0) -> np.ndarray:
+    """Dense kernel block on the device (kernels.py:494-530, no nugget);
+    radius > 0: great-circle distance, points as (lon, lat) degrees."""
     lib = _lib.load()
     a = np.ascontiguousarray(rows_xy, dtype=np.float64)
     b = np.ascontiguousarray(cols_xy, dtype=np.float64)
     out = np.empty((b.shape[0], a.shape[0]))  # column-major m x n == row-major n x m
-    rc = lib.tlrb_matern_block(dptr(a), a.shape[0], dptr(b), b.shape[0], p.theta1, p.theta2,
-                               p.theta3, dptr(out), 0)
+    rc = lib.tlrb_matern_block_metric(dptr(a), a.shape[0], dptr(b), b.shape[0], p.theta1, p.theta2,
+                                      p.theta3, float(radius), dptr(out), 0)
     if rc:
         raise ValueError(f"tlrb_matern_block failed ({rc})")
     return out.T.copy()

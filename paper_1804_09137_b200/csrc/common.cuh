@@ -71,6 +71,14 @@ struct MaternParamsDev {
 };
 MaternParamsDev make_matern(double theta1, double theta2, double nu);
 
+// Point coordinates in the layout the distance kernel reads (the reference's
+// KernelView, geometry.py:58-72,106-122): Euclidean a1 = x, a2 = y; great
+// circle a1 = lat (rad), a2 = lon (rad), a3 = cos(lat), diam = 2 * radius.
+struct Pts {
+  const double* a1; const double* a2; const double* a3;
+  double diam;            // 0 => Euclidean
+};
+
 struct GenTile {          // one Matern block: rows [r0, r0+m) x cols [c0, c0+n)
   double* out; int ld;
   int r0, m, c0, n;
@@ -141,8 +149,8 @@ class DescArena {
 };
 
 // launchers (all asynchronous on `s`)
-void launch_gen_tiles(const std::vector<GenTile>& tiles, const double* x, const double* y,
-                      const MaternParamsDev& p, DescArena& ar, cudaStream_t s);
+void launch_gen_tiles(const std::vector<GenTile>& tiles, const Pts& pts, const MaternParamsDev& p,
+                      DescArena& ar, cudaStream_t s);
 void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s);
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);
@@ -157,9 +165,8 @@ void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sum_log(const double* logdiag, int n, double* out, cudaStream_t s);
 void launch_dot(const double* x, int n, double* out, cudaStream_t s);
-void launch_cross_gemv(const double* kx, const double* ky, const double* w, int64_t n,
-                       const double* ux, const double* uy, int64_t m, const MaternParamsDev& p,
-                       double* partial, double* out, cudaStream_t s);
+void launch_cross_gemv(const Pts& known, const double* w, int64_t n, const Pts& unknown, int64_t m,
+                       const MaternParamsDev& p, double* partial, double* out, cudaStream_t s);
 void launch_aux(const double* sums, const int* kinds, int nprob, double* aux, int* ok,
                 double rel_tol2, cudaStream_t s);
 

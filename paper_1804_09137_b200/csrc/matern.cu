@@ -130,6 +130,23 @@ __device__ __forceinline__ double matern_t(const MaternParamsDev& p, double t) {
   return v;
 }
 
+// Distance between two points in the Pts layout.  Great circle: haversine in
+// the reference's operation order (kernels.py:461-473); Euclidean:
+// kernels.py:436-443.  `diam` is uniform across the grid, so the branch never
+// diverges.
+__device__ __forceinline__ double pair_dist(double diam, double p1, double p2, double p3, double q1,
+                                            double q2, double q3) {
+  if (diam > 0.0) {
+    const double sp = sin(0.5 * (q1 - p1));
+    const double sl = sin(0.5 * (q2 - p2));
+    double a = sp * sp + p3 * q3 * sl * sl;
+    if (a > 1.0) a = 1.0;
+    return diam * asin(sqrt(a));
+  }
+  const double dx = p1 - q1, dy = p2 - q2;
+  return sqrt(dx * dx + dy * dy);
+}
+
 // ---------------------------------------------------------------- K1 tiles
 // Each CTA writes a 64 (rows) x 32 (cols) block of one tile, column-major, so
 // a warp's stores are 32 consecutive doubles (256 B, fully coalesced).
@@ -137,9 +154,7 @@ constexpr int GEN_BM = 64, GEN_BN = 32;
 
 __global__ void __launch_bounds__(256) gen_tiles_kernel(const GenTile* __restrict__ tiles,
                                                         const int* __restrict__ start, int ntiles,
-                                                        const double* __restrict__ X,
-                                                        const double* __restrict__ Y,
-                                                        MaternParamsDev p) {
+                                                        Pts P, MaternParamsDev p) {
   const int blk = blockIdx.x;
   int lo = 0, hi = ntiles - 1;
   while (lo < hi) {
@@ -153,22 +168,22 @@ __global__ void __launch_bounds__(256) gen_tiles_kernel(const GenTile* __restric
   const int r = bm * GEN_BM + (threadIdx.x & 63);
   if (r >= T.m) return;
   const int gr = T.r0 + r;
-  const double px = X[gr], py = Y[gr];
+  const double p1 = P.a1[gr], p2 = P.a2[gr], p3 = P.diam > 0.0 ? P.a3[gr] : 0.0;
   const int cbase = bn * GEN_BN + (threadIdx.x >> 6) * (GEN_BN / 4);
 #pragma unroll
   for (int cc = 0; cc < GEN_BN / 4; ++cc) {
     const int c = cbase + cc;
     if (c >= T.n) break;
     const int gc = T.c0 + c;
-    const double dx = px - X[gc], dy = py - Y[gc];
-    double v = matern_t(p, sqrt(dx * dx + dy * dy) * p.inv_theta2);
+    const double q3 = P.diam > 0.0 ? P.a3[gc] : 0.0;
+    double v = matern_t(p, pair_dist(P.diam, p1, p2, p3, P.a1[gc], P.a2[gc], q3) * p.inv_theta2);
     if (gr == gc) v += T.diag_add;
     T.out[(size_t)c * T.ld + r] = v;
   }
 }
 
-void launch_gen_tiles(const std::vector<GenTile>& tiles, const double* x, const double* y,
-                      const MaternParamsDev& p, DescArena& ar, cudaStream_t s) {
+void launch_gen_tiles(const std::vector<GenTile>& tiles, const Pts& pts, const MaternParamsDev& p,
+                      DescArena& ar, cudaStream_t s) {
   if (tiles.empty()) return;
   std::vector<int> start(tiles.size() + 1);
   int tot = 0;
@@ -183,7 +198,7 @@ void launch_gen_tiles(const std::vector<GenTile>& tiles, const double* x, const 
   double by = 0;
   for (const GenTile& t : tiles) by += 8.0 * t.m * t.n;
   ProfScope ps(K_GEN, s, 0, by);
-  gen_tiles_kernel<<<tot, 256, 0, s>>>(dt, ds, (int)tiles.size(), x, y, p);
+  gen_tiles_kernel<<<tot, 256, 0, s>>>(dt, ds, (int)tiles.size(), pts, p);
   post_launch();
 }
 
@@ -205,20 +220,16 @@ void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStrea
 // never materialised (predict.py:77-79 builds it densely).
 constexpr int XG_CHUNK = 2048;
 
-__global__ void __launch_bounds__(256) cross_gemv_kernel(const double* __restrict__ kx,
-                                                         const double* __restrict__ ky,
-                                                         const double* __restrict__ w, int64_t n,
-                                                         const double* __restrict__ ux,
-                                                         const double* __restrict__ uy,
-                                                         MaternParamsDev p, double* partial) {
+__global__ void __launch_bounds__(256) cross_gemv_kernel(Pts K, const double* __restrict__ w, int64_t n,
+                                                         Pts U, MaternParamsDev p, double* partial) {
   const int a = blockIdx.y;
   const int chunk = blockIdx.x;
   const int64_t j0 = (int64_t)chunk * XG_CHUNK;
-  const double px = ux[a], py = uy[a];
+  const double p1 = U.a1[a], p2 = U.a2[a], p3 = U.diam > 0.0 ? U.a3[a] : 0.0;
   double acc = 0.0;
   for (int64_t j = j0 + threadIdx.x; j < n && j < j0 + XG_CHUNK; j += blockDim.x) {
-    const double dx = px - kx[j], dy = py - ky[j];
-    acc += matern_t(p, sqrt(dx * dx + dy * dy) * p.inv_theta2) * w[j];
+    const double q3 = K.diam > 0.0 ? K.a3[j] : 0.0;
+    acc += matern_t(p, pair_dist(K.diam, p1, p2, p3, K.a1[j], K.a2[j], q3) * p.inv_theta2) * w[j];
   }
   __shared__ double red[256];
   red[threadIdx.x] = acc;
@@ -238,13 +249,12 @@ __global__ void row_sum_kernel(const double* partial, int nchunk, int64_t m, dou
   out[a] = s;
 }
 
-void launch_cross_gemv(const double* kx, const double* ky, const double* w, int64_t n,
-                       const double* ux, const double* uy, int64_t m, const MaternParamsDev& p,
-                       double* partial, double* out, cudaStream_t s) {
+void launch_cross_gemv(const Pts& known, const double* w, int64_t n, const Pts& unknown, int64_t m,
+                       const MaternParamsDev& p, double* partial, double* out, cudaStream_t s) {
   const int nchunk = (int)((n + XG_CHUNK - 1) / XG_CHUNK);
   dim3 grid(nchunk, (unsigned)m);
   ProfScope ps(K_CROSS, s, 2.0 * n * m, 24.0 * n);
-  cross_gemv_kernel<<<grid, 256, 0, s>>>(kx, ky, w, n, ux, uy, p, partial);
+  cross_gemv_kernel<<<grid, 256, 0, s>>>(known, w, n, unknown, p, partial);
   post_launch();
   row_sum_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(partial, nchunk, m, out);
   post_launch();

@@ -52,8 +52,12 @@ struct tlrb_handle {
   int64_t n = 0;
   int nb = 0, t = 0, cap = 0, max_rank = 0;
   std::vector<int> off, sz;
-  double* dx = nullptr;
+  double* dx = nullptr;          // point coordinates in the Pts layout (a1, a2, a3)
   double* dy = nullptr;
+  double* dz = nullptr;          // cos(lat), great circle only
+  double diam = 0.0;             // 2 * sphere radius; 0 => Euclidean
+  std::vector<double> hxy;       // caller's (x, y) / (lon, lat), kept for tlrb_set_metric
+  Pts pts() const { return Pts{dx, dy, dz, diam}; }
   double* diag = nullptr;
   // tile factors: rank-adaptive bump arena, reset at every factorisation;
   // tile t owns U (nb x tcap[t]) and V (nb x tcap[t]), or a dense nb x nb
@@ -70,7 +74,7 @@ struct tlrb_handle {
   double* d_w = nullptr;         // solve temporaries (t * nb)
   double* d_y = nullptr;         // y = L x output (n), allocated on first use
   // kriging
-  double* d_ux = nullptr; double* d_uy = nullptr; double* d_pred = nullptr;
+  double* d_ux = nullptr; double* d_uy = nullptr; double* d_uz = nullptr; double* d_pred = nullptr;
   double* d_partial = nullptr; int64_t ucap = 0;
   DescArena ar;
   // compression workspace
@@ -351,7 +355,7 @@ void generate(tlrb_handle* h, double nugget, bool dense_lower) {
       for (int j = 0; j < i; ++j)  // L_ij^T: rows = tile j points, cols = tile i points
         if (h->own(i, j)) tiles.push_back({h->Ut(i, j), h->nb, h->off[j], h->sz[j], h->off[i], h->sz[i], 0.0});
   }
-  launch_gen_tiles(tiles, h->dx, h->dy, h->mp, h->ar, h->stream);
+  launch_gen_tiles(tiles, h->pts(), h->mp, h->ar, h->stream);
   for (int i = 0; i < h->t; ++i) {
     h->work.add(0, 8.0 * h->sz[i] * h->sz[i]);
     if (dense_lower)
@@ -384,7 +388,7 @@ void compress_all(tlrb_handle* h, double acc) {
       jobs.push_back(J);
       gen.push_back({J.M, J.m, h->off[i], J.m, h->off[j], J.n, 0.0});
     }
-    launch_gen_tiles(gen, h->dx, h->dy, h->mp, h->ar, h->stream);
+    launch_gen_tiles(gen, h->pts(), h->mp, h->ar, h->stream);
     compress_jobs(h, jobs, acc);
     for (size_t q = c0; q < c1; ++q) {
       const Job& J = jobs[q - c0];
@@ -943,6 +947,29 @@ void backward_solve(tlrb_handle* h) {
 }
 
 // -------------------------------------------------------------- one eval
+// Host half of the reference's KernelView (geometry.py:106-122): Euclidean
+// keeps (x, y); great circle maps (lon, lat) degrees to (lat, lon) radians and
+// cos(lat), after the range check of LocationSet.__init__ (geometry.py:86-90).
+int kernel_view(const double* xy, int64_t n, double radius, std::vector<double>& a1, std::vector<double>& a2,
+                std::vector<double>& a3) {
+  if (!(radius >= 0.0) || !std::isfinite(radius)) return TLRB_ERR_ARG;
+  a1.resize(n); a2.resize(n); a3.clear();
+  if (radius == 0.0) {
+    for (int64_t i = 0; i < n; ++i) { a1[i] = xy[2 * i]; a2[i] = xy[2 * i + 1]; }
+    return TLRB_OK;
+  }
+  a3.resize(n);
+  const double deg = M_PI / 180.0;   // numpy.radians: x * (pi / 180)
+  for (int64_t i = 0; i < n; ++i) {
+    const double lon = xy[2 * i], lat = xy[2 * i + 1];
+    if (std::fabs(lon) > 180.0 || std::fabs(lat) > 90.0) return TLRB_ERR_ARG;
+    a1[i] = lat * deg;
+    a2[i] = lon * deg;
+    a3[i] = std::cos(a1[i]);
+  }
+  return TLRB_OK;
+}
+
 int validate(double th1, double th2, double th3, double nugget, double acc) {
   const double v[5] = {th1, th2, th3, nugget, acc};
   for (double x : v)
@@ -1093,8 +1120,9 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
       h->off.push_back(i * h->nb);
       h->sz.push_back((int)std::min<int64_t>(h->nb, n - (int64_t)i * h->nb));
     }
-    std::vector<double> xs(n), ys(n);
-    for (int64_t i = 0; i < n; ++i) { xs[i] = xy[2 * i]; ys[i] = xy[2 * i + 1]; }
+    h->hxy.assign(xy, xy + 2 * n);
+    std::vector<double> xs, ys, zs;
+    kernel_view(xy, n, 0.0, xs, ys, zs);
     TLRB_CUDA(cudaMalloc(&h->dx, n * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->dy, n * sizeof(double)));
     TLRB_CUDA(cudaMemcpy(h->dx, xs.data(), n * sizeof(double), cudaMemcpyHostToDevice));
@@ -1195,7 +1223,7 @@ void tlrb_destroy(tlrb_handle* h) {
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->d_ibuf) cudaFree(h->d_ibuf);
   if (h->d_acc) cudaFree(h->d_acc);
-  void* ptrs[] = {h->dx, h->dy, h->diag, h->arena, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
+  void* ptrs[] = {h->dx, h->dy, h->dz, h->d_uz, h->diag, h->arena, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
                   h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_y, h->d_ux, h->d_uy,
                   h->d_pred, h->d_partial};
   for (void* p : ptrs)
@@ -1275,24 +1303,28 @@ int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown, 
     TLRB_CUDA(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
     if (m > h->ucap) {
-      if (h->d_ux) { cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_pred); cudaFree(h->d_partial); }
+      if (h->d_ux) { cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_uz); cudaFree(h->d_pred); cudaFree(h->d_partial); }
       h->ucap = m;
       const int64_t nchunk = (h->n + 2047) / 2048;
       TLRB_CUDA(cudaMalloc(&h->d_ux, m * sizeof(double)));
       TLRB_CUDA(cudaMalloc(&h->d_uy, m * sizeof(double)));
+      TLRB_CUDA(cudaMalloc(&h->d_uz, m * sizeof(double)));
       TLRB_CUDA(cudaMalloc(&h->d_pred, m * sizeof(double)));
       TLRB_CUDA(cudaMalloc(&h->d_partial, m * nchunk * sizeof(double)));
     }
-    std::vector<double> ux(m), uy(m);
-    for (int64_t i = 0; i < m; ++i) { ux[i] = xy_unknown[2 * i]; uy[i] = xy_unknown[2 * i + 1]; }
+    std::vector<double> ux, uy, uz;
+    if (kernel_view(xy_unknown, m, 0.5 * h->diam, ux, uy, uz)) return TLRB_ERR_ARG;
     TLRB_CUDA(cudaMemcpyAsync(h->d_ux, ux.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
     TLRB_CUDA(cudaMemcpyAsync(h->d_uy, uy.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (h->diam > 0.0)
+      TLRB_CUDA(cudaMemcpyAsync(h->d_uz, uz.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
     TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double), cudaMemcpyHostToDevice, s));
     int r = factorize(h, th1, th2, th3, nugget, acc);
     if (r) return r;
     forward_solve(h);
     backward_solve(h);
-    launch_cross_gemv(h->dx, h->dy, h->d_z, h->n, h->d_ux, h->d_uy, m, h->mp, h->d_partial, h->d_pred, s);
+    launch_cross_gemv(h->pts(), h->d_z, h->n, Pts{h->d_ux, h->d_uy, h->d_uz, h->diam}, m, h->mp,
+                      h->d_partial, h->d_pred, s);
     TLRB_CUDA(cudaMemcpyAsync(pred, h->d_pred, m * sizeof(double), cudaMemcpyDeviceToHost, s));
     h->sync();
     return TLRB_OK;
@@ -1340,29 +1372,60 @@ int32_t tlrb_bessel_k(double nu, const double* x, int64_t count, double* out, in
 
 int32_t tlrb_matern_block(const double* rows_xy, int64_t m, const double* cols_xy, int64_t n, double th1,
                           double th2, double th3, double* out, int32_t device) {
+  return tlrb_matern_block_metric(rows_xy, m, cols_xy, n, th1, th2, th3, 0.0, out, device);
+}
+
+int32_t tlrb_matern_block_metric(const double* rows_xy, int64_t m, const double* cols_xy, int64_t n,
+                                 double th1, double th2, double th3, double sphere_radius, double* out,
+                                 int32_t device) {
   if (!rows_xy || !cols_xy || !out || m < 1 || n < 1) return TLRB_ERR_ARG;
   if (validate(th1, th2, th3, 0.0, 0.0)) return TLRB_ERR_ARG;
+  std::vector<double> all(2 * (m + n));
+  std::copy(rows_xy, rows_xy + 2 * m, all.begin());
+  std::copy(cols_xy, cols_xy + 2 * n, all.begin() + 2 * m);
+  std::vector<double> a1, a2, a3;
+  if (kernel_view(all.data(), m + n, sphere_radius, a1, a2, a3)) return TLRB_ERR_ARG;
   return guarded(nullptr, [&]() -> int {
     TLRB_CUDA(cudaSetDevice(device));
-    std::vector<double> xs(m + n), ys(m + n);
-    for (int64_t i = 0; i < m; ++i) { xs[i] = rows_xy[2 * i]; ys[i] = rows_xy[2 * i + 1]; }
-    for (int64_t i = 0; i < n; ++i) { xs[m + i] = cols_xy[2 * i]; ys[m + i] = cols_xy[2 * i + 1]; }
-    double *px, *py, *po;
-    TLRB_CUDA(cudaMalloc(&px, (m + n) * 8));
-    TLRB_CUDA(cudaMalloc(&py, (m + n) * 8));
+    double *p1, *p2, *p3 = nullptr, *po;
+    TLRB_CUDA(cudaMalloc(&p1, (m + n) * 8));
+    TLRB_CUDA(cudaMalloc(&p2, (m + n) * 8));
     TLRB_CUDA(cudaMalloc(&po, m * n * 8));
-    TLRB_CUDA(cudaMemcpy(px, xs.data(), (m + n) * 8, cudaMemcpyHostToDevice));
-    TLRB_CUDA(cudaMemcpy(py, ys.data(), (m + n) * 8, cudaMemcpyHostToDevice));
+    TLRB_CUDA(cudaMemcpy(p1, a1.data(), (m + n) * 8, cudaMemcpyHostToDevice));
+    TLRB_CUDA(cudaMemcpy(p2, a2.data(), (m + n) * 8, cudaMemcpyHostToDevice));
+    if (!a3.empty()) {
+      TLRB_CUDA(cudaMalloc(&p3, (m + n) * 8));
+      TLRB_CUDA(cudaMemcpy(p3, a3.data(), (m + n) * 8, cudaMemcpyHostToDevice));
+    }
     DescArena ar;
     ar.init(1 << 20);
     // diag_add applies where global row == global col: rows and cols are disjoint index ranges here
-    launch_gen_tiles({GenTile{po, (int)m, 0, (int)m, (int)m, (int)n, 0.0}}, px, py, make_matern(th1, th2, th3),
-                     ar, 0);
+    launch_gen_tiles({GenTile{po, (int)m, 0, (int)m, (int)m, (int)n, 0.0}}, Pts{p1, p2, p3, 2.0 * sphere_radius},
+                     make_matern(th1, th2, th3), ar, 0);
     TLRB_CUDA(cudaMemcpy(out, po, m * n * 8, cudaMemcpyDeviceToHost));
     ar.release();
-    cudaFree(px);
-    cudaFree(py);
+    cudaFree(p1);
+    cudaFree(p2);
+    if (p3) cudaFree(p3);
     cudaFree(po);
+    return TLRB_OK;
+  });
+}
+
+int32_t tlrb_set_metric(tlrb_handle* h, double sphere_radius) {
+  if (!h) return TLRB_ERR_ARG;
+  std::vector<double> a1, a2, a3;
+  if (kernel_view(h->hxy.data(), h->n, sphere_radius, a1, a2, a3)) return TLRB_ERR_ARG;
+  return guarded(h, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(h->device));
+    TLRB_CUDA(cudaStreamSynchronize(h->stream));
+    TLRB_CUDA(cudaMemcpy(h->dx, a1.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
+    TLRB_CUDA(cudaMemcpy(h->dy, a2.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
+    if (!a3.empty()) {
+      if (!h->dz) TLRB_CUDA(cudaMalloc(&h->dz, h->n * sizeof(double)));
+      TLRB_CUDA(cudaMemcpy(h->dz, a3.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    h->diam = 2.0 * sphere_radius;
     return TLRB_OK;
   });
 }

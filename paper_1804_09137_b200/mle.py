@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .api import LikelihoodConfig, MaternParams, NotPositiveDefiniteError, _coords_of, _handle_for
+from .api import LikelihoodConfig, MaternParams, NotPositiveDefiniteError, _coords_of, _handle_for, _radius_of
 
 
 @dataclass(frozen=True)
@@ -63,7 +63,7 @@ def mle_fit(locs, z, cfg: LikelihoodConfig, objective=None, max_evaluations: int
     hi = np.array([b[1] for b in bounds])
     if objective is None:
         coords = _coords_of(locs)
-        h = _handle_for(coords, min(cfg.tile_size(), len(locs)), cfg.max_rank, cfg.ngpus)
+        h = _handle_for(coords, min(cfg.tile_size(), len(locs)), cfg.max_rank, cfg.ngpus, _radius_of(locs))
         acc = cfg.accuracy if cfg.mode == "tlr" else None
         zz = np.ascontiguousarray(z, dtype=float)
 
