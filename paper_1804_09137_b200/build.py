@@ -12,6 +12,8 @@ OUT = PKG / "libtlrb200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+if os.environ.get("TLRB_CLOCK_PROF") == "1":   # clock64 phase counters (rebuild with --force)
+    FLAGS.append("-DTLRB_CLOCK_PROF")
 
 
 def needs_build() -> bool:

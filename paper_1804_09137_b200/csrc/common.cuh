@@ -40,7 +40,8 @@ struct Profiler {
   bool on = false;
   double ms[K_NCLASS] = {}, flops[K_NCLASS] = {}, bytes[K_NCLASS] = {};
   int64_t count[K_NCLASS] = {};
-  struct Pend { int cls; cudaEvent_t a, b; };
+  struct Pend { int cls; cudaEvent_t a, b; cudaStream_t s; };
+  cudaEvent_t epoch = nullptr;   // TLRB_TIMELINE=path: per-launch (class, start, end) dump
   std::vector<Pend> pend;
   std::vector<cudaEvent_t> pool;
   int open_cls = -1;
@@ -60,6 +61,16 @@ struct ProfScope {   // RAII: times one launch of class cls
   }
   ~ProfScope() { if (g_prof.on) g_prof.end(s, fl, by); }
 };
+
+// clock64 phase counters inside the QRCP / Jacobi kernels (TLRB_QRCP_PROF /
+// TLRB_JACOBI_PROF readouts); compiled in only with -DTLRB_CLOCK_PROF
+// (TLRB_CLOCK_PROF=1 python -m paper_1804_09137_b200.build --force), as the
+// live counters cost registers in the hot loops.
+#ifdef TLRB_CLOCK_PROF
+constexpr bool kClockProf = true;
+#else
+constexpr bool kClockProf = false;
+#endif
 
 // ------------------------------------------------------------------ Matern
 struct MaternParamsDev {
@@ -92,6 +103,7 @@ struct GemmProb {
   int ta, tb;             // op(A) = A^T if ta, op(B) = B^T if tb
   int lower_only;         // skip CTA tiles strictly above the diagonal
   double alpha, beta;     // C = alpha op(A) op(B) + beta Cin
+  const int* active = nullptr;   // optional device flag: skip the problem when *active == 0
 };
 
 // --------------------------------------------------------------------- TRSM
@@ -153,6 +165,10 @@ void launch_gen_tiles(const std::vector<GenTile>& tiles, const Pts& pts, const M
                       DescArena& ar, cudaStream_t s);
 void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s);
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
+// multi-launch staging: build several batches on the host, upload once, launch
+struct GemmStaged { int poff = 0, soff = 0, n = 0, tot = 0; double fl = 0, by = 0; };
+GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls);
+void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s);
 void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
@@ -160,6 +176,7 @@ void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
 // gathered[p] = 1: columns left in place (R column jj at perm[jj]); 0: physically pivoted
 void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered, DescArena& ar,
                  cudaStream_t s);
+void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(128) dgemm_vbatch_kernel(const GemmProb* __res
     if (start[mid] <= blk) lo = mid; else hi = mid - 1;
   }
   const GemmProb P = probs[lo];
+  if (P.active && !*P.active) return;
   const int local = blk - start[lo];
   const int tm = (P.m + GBM - 1) / GBM;
   const int m0 = (local % tm) * GBM, n0 = (local / tm) * GBN;
@@ -130,31 +131,46 @@ __global__ void __launch_bounds__(128) dgemm_vbatch_kernel(const GemmProb* __res
   }
 }
 
-void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
-  if (probs.empty()) return;
-  std::vector<GemmProb> keep;
-  keep.reserve(probs.size());
-  std::vector<int> start;
-  start.reserve(probs.size() + 1);
+// host-side staging of one batched launch: appends the non-empty problems and
+// their tile prefix sums to (allp, alls); returns the launch record
+GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls) {
+  GemmStaged g;
+  g.poff = (int)allp.size();
+  g.soff = (int)alls.size();
   int tot = 0;
   for (const GemmProb& p : probs) {
     if (p.m <= 0 || p.n <= 0) continue;
-    keep.push_back(p);
-    start.push_back(tot);
+    allp.push_back(p);
+    alls.push_back(tot);
     tot += ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
+    g.fl += 2.0 * p.m * p.n * p.k;
+    g.by += 8.0 * ((double)p.m * p.k + (double)p.k * p.n + (double)p.m * p.n * (p.beta != 0.0 ? 2 : 1));
   }
-  if (tot == 0) return;
-  start.push_back(tot);
+  alls.push_back(tot);
+  g.n = (int)allp.size() - g.poff;
+  g.tot = tot;
+  return g;
+}
+
+// launch a staged batch whose descriptors already live on the device
+void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s) {
+  if (g.tot == 0 || g.n == 0) return;
+  ProfScope ps(K_GEMM, s, g.fl, g.by);
+  dgemm_vbatch_kernel<<<g.tot, 128, 0, s>>>(dp + g.poff, ds + g.soff, g.n);
+  post_launch();
+}
+
+void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  std::vector<GemmProb> keep;
+  std::vector<int> start;
+  keep.reserve(probs.size());
+  start.reserve(probs.size() + 1);
+  const GemmStaged g = stage_gemm(probs, keep, start);
+  if (g.tot == 0) return;
   const GemmProb* dp = ar.put(keep, s);
   const int* ds = ar.put(start, s);
-  double fl = 0, by = 0;
-  for (const GemmProb& p : keep) {
-    fl += 2.0 * p.m * p.n * p.k;
-    by += 8.0 * ((double)p.m * p.k + (double)p.k * p.n + (double)p.m * p.n * (p.beta != 0.0 ? 2 : 1));
-  }
-  ProfScope ps(K_GEMM, s, fl, by);
-  dgemm_vbatch_kernel<<<tot, 128, 0, s>>>(dp, ds, (int)keep.size());
-  post_launch();
+  launch_gemm_staged(g, dp, ds, s);
 }
 
 }  // namespace tlrb

@@ -37,13 +37,8 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-constexpr bool kPipelined = false;   // per-column producer/consumer barriers (experimental)
-
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-__device__ __forceinline__ void named_arrive(int id, int threads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // round-robin tournament over nplayers (even): match idx of round r
@@ -76,11 +71,17 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return y;
 }
 
-// Cross rotation of a register-resident column xa (rows lane + 32 i) with a
-// register copy xb; returns true if rotated (al, be updated).
+// Rotation of a register-resident column pair stored in SCALED form: the true
+// columns are a_p = dp * xa, a_q = dq * xb (ip = 1/dp, iq = 1/dq).  The
+// rotation [a_p a_q] <- [c a_p - s a_q, s a_p + c a_q] is applied as
+//   xa <- xa - t (dq/dp) xb,  xb <- xb + t (dp/dq) xa,  dp, dq <- c dp, c dq
+// (modified / fast Givens, as LAPACK dgesvj's drotm path): one FMA per
+// element and the cosine off the element-update chain.  al, be are the true
+// squared norms.  Returns true if rotated.
 template <int RPL>
 __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL], double& al, double& be,
-                                            double tol, double tiny2) {
+                                            double& dp, double& ip, double& dq, double& iq, double tol,
+                                            double tiny2) {
   if (al <= tiny2 || be <= tiny2) return false;
   double g0 = 0.0, g1 = 0.0;
 #pragma unroll
@@ -88,7 +89,7 @@ __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL]
     g0 = fma(xa[i], xb[i], g0);
     if (i + 1 < RPL) g1 = fma(xa[i + 1], xb[i + 1], g1);
   }
-  const double ga = wsum(g0 + g1);
+  const double ga = wsum(g0 + g1) * (dp * dq);
   if (ga == 0.0 || ga * ga <= (tol * tol) * (al * be)) return false;
   // t = sign(zeta)/(|zeta| + sqrt(1+zeta^2)), zeta = (be-al)/(2ga), written
   // with one reciprocal: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)).  The
@@ -98,20 +99,88 @@ __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL]
   const double q2 = fma(d, d, g2 * g2);
   const double hyp = q2 * fast_rsqrt(q2);
   const double t = (d >= 0.0 ? g2 : -g2) * fast_rcp(fabs(d) + hyp);
-  const double c = fast_rsqrt(fma(t, t, 1.0));
-  const double sn = c * t;
+  const double mup = t * (dq * ip), muq = t * (dp * iq);
 #pragma unroll
   for (int i = 0; i < RPL; ++i) {
     const double x = xa[i], y = xb[i];
-    xa[i] = fma(c, x, -sn * y);
-    xb[i] = fma(sn, x, c * y);
+    xa[i] = fma(-mup, y, x);
+    xb[i] = fma(muq, x, y);
   }
+  const double u = fma(t, t, 1.0);
+  const double c = fast_rsqrt(u), ic = u * c;   // cos, 1/cos
+  dp *= c; dq *= c; ip *= ic; iq *= ic;
   al = fma(-t, ga, al);
   be = fma(t, ga, be);
   return true;
 }
 
-template <int RPL, int NT>
+// Column state of a staged column: true squared norm, scale, 1/scale.
+struct ColSt {
+  double n2, d, id;
+};
+
+// Two independent scaled rotations (a0, b0) and (a1, b1) interleaved for ILP:
+// both dot products / shuffle trees / rotation parameter chains overlap.
+// Branch-free: a pair that needs no rotation gets t = 0, which leaves its
+// columns bit-identical (fma(-0, y, x) = x).  r0 / r1 report rotations.
+template <int RPL>
+__device__ __forceinline__ void rotate2(double (&a0)[RPL], double (&b0)[RPL], double (&a1)[RPL], double (&b1)[RPL],
+                                        ColSt& A0, ColSt& B0, ColSt& A1, ColSt& B1, double tol, double tiny2,
+                                        bool& r0, bool& r1) {
+  double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPL; i += 2) {
+    g00 = fma(a0[i], b0[i], g00);
+    g10 = fma(a1[i], b1[i], g10);
+    if (i + 1 < RPL) {
+      g01 = fma(a0[i + 1], b0[i + 1], g01);
+      g11 = fma(a1[i + 1], b1[i + 1], g11);
+    }
+  }
+  double h0 = g00 + g01, h1 = g10 + g11;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    h0 += __shfl_xor_sync(0xffffffffu, h0, o);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+  }
+  const double ga0 = h0 * (A0.d * B0.d), ga1 = h1 * (A1.d * B1.d);
+  const double tol2 = tol * tol;
+  r0 = A0.n2 > tiny2 && B0.n2 > tiny2 && ga0 != 0.0 && ga0 * ga0 > tol2 * (A0.n2 * B0.n2);
+  r1 = A1.n2 > tiny2 && B1.n2 > tiny2 && ga1 != 0.0 && ga1 * ga1 > tol2 * (A1.n2 * B1.n2);
+  // t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)), d = beta - alpha, g2 = 2 gamma
+  const double d0 = B0.n2 - A0.n2, d1 = B1.n2 - A1.n2;
+  const double e0 = 2.0 * ga0, e1 = 2.0 * ga1;
+  const double q0 = r0 ? fma(d0, d0, e0 * e0) : 1.0, q1 = r1 ? fma(d1, d1, e1 * e1) : 1.0;
+  const double y0 = q0 * fast_rsqrt(q0), y1 = q1 * fast_rsqrt(q1);
+  double t0 = (d0 >= 0.0 ? e0 : -e0) * fast_rcp(fabs(d0) + y0);
+  double t1 = (d1 >= 0.0 ? e1 : -e1) * fast_rcp(fabs(d1) + y1);
+  t0 = r0 ? t0 : 0.0;
+  t1 = r1 ? t1 : 0.0;
+  const double mp0 = t0 * (B0.d * A0.id), mq0 = t0 * (A0.d * B0.id);
+  const double mp1 = t1 * (B1.d * A1.id), mq1 = t1 * (A1.d * B1.id);
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const double x0 = a0[i], y0_ = b0[i], x1 = a1[i], y1_ = b1[i];
+    a0[i] = fma(-mp0, y0_, x0);
+    b0[i] = fma(mq0, x0, y0_);
+    a1[i] = fma(-mp1, y1_, x1);
+    b1[i] = fma(mq1, x1, y1_);
+  }
+  if (r0) {
+    const double u = fma(t0, t0, 1.0), c = fast_rsqrt(u), ic = u * c;
+    A0.d *= c; B0.d *= c; A0.id *= ic; B0.id *= ic;
+    A0.n2 = fma(-t0, ga0, A0.n2);
+    B0.n2 = fma(t0, ga0, B0.n2);
+  }
+  if (r1) {
+    const double u = fma(t1, t1, 1.0), c = fast_rsqrt(u), ic = u * c;
+    A1.d *= c; B1.d *= c; A1.id *= ic; B1.id *= ic;
+    A1.n2 = fma(-t1, ga1, A1.n2);
+    B1.n2 = fma(t1, ga1, B1.n2);
+  }
+}
+
+template <int RPL, int NT, int K>
 __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
                                                              int max_sweeps) {
   extern __shared__ double sm[];
@@ -122,9 +191,13 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   const int m = P.m, s = P.s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nthr = blockDim.x;
+  // columns are staged with a padded stride MP = 32 RPL (rows >= m are zero
+  // and stay zero under rotations), so register loads / stores need no bounds
+  constexpr int MP = 32 * RPL;
   double* S0 = sm;
-  double* S1 = sm + (size_t)B * m;
-  __shared__ double nrm[2][16];      // maintained squared column norms of S0 / S1
+  double* S1 = sm + (size_t)B * MP;
+  __shared__ double nrm[2][16];      // maintained true squared column norms of S0 / S1
+  __shared__ double scl[2][16], iscl[2][16];   // column scales (true column = scl * stored)
   __shared__ int rot_flag;
   // rotation tolerance: LAPACK dgesvj's m*eps, tightened for very small acc
   // (the truncated product M V V^T inherits the columns' non-orthogonality);
@@ -144,90 +217,171 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   auto load = [&](double* dst, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     if (vec) {
-      const int mh = m >> 1;
-      for (int e = threadIdx.x; e < mh * B; e += nthr) {
-        const int c = e / mh, r = 2 * (e - c * mh);
-        double* d = dst + c * m + r;
+      for (int c = warp; c < B; c += nw) {
+        double* d = dst + c * MP;
         if (c < nc) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                       "l"(P.X + (size_t)(c0 + c) * P.ldx + r));
+          const double* src = P.X + (size_t)(c0 + c) * P.ldx;
+          for (int r = 2 * lane; r < m; r += 64) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(d + r);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + r));
+          }
         } else {
-          d[0] = 0.0;
-          d[1] = 0.0;
+          for (int r = lane; r < m; r += 32) d[r] = 0.0;
         }
       }
       asm volatile("cp.async.commit_group;\n" ::);
     } else {
-      for (int e = threadIdx.x; e < m * B; e += nthr) {
-        const int c = e / m, r = e - c * m;
-        dst[c * m + r] = (c < nc) ? __ldcg(P.X + (size_t)(c0 + c) * P.ldx + r) : 0.0;
+      for (int c = warp; c < B; c += nw) {
+        const double* src = P.X + (size_t)(c0 + c) * P.ldx;
+        for (int r = lane; r < m; r += 32) dst[c * MP + r] = (c < nc) ? __ldcg(src + r) : 0.0;
       }
     }
   };
   auto cp_wait = [&]() {
     if (vec) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   };
-  auto norms_of = [&](const double* src, double* nr) {
+  // true squared norms of a freshly loaded block (scales reset to 1)
+  auto norms_of = [&](const double* src, int slot) {
     for (int c = warp; c < B; c += nw) {
       double a0 = 0.0, a1 = 0.0;
-      int r = lane;
-      for (; r + 32 < m; r += 64) {
-        a0 = fma(src[c * m + r], src[c * m + r], a0);
-        a1 = fma(src[c * m + r + 32], src[c * m + r + 32], a1);
+#pragma unroll
+      for (int i = 0; i < RPL; i += 2) {
+        const double x0 = src[c * MP + lane + 32 * i];
+        a0 = fma(x0, x0, a0);
+        if (i + 1 < RPL) {
+          const double x1 = src[c * MP + lane + 32 * (i + 1)];
+          a1 = fma(x1, x1, a1);
+        }
       }
-      if (r < m) a0 = fma(src[c * m + r], src[c * m + r], a0);
       const double a = wsum(a0 + a1);
-      if (lane == 0) nr[c] = a;
+      if (lane == 0) { nrm[slot][c] = a; scl[slot][c] = 1.0; iscl[slot][c] = 1.0; }
     }
   };
-  auto store = [&](const double* src, int blk) {
+  // write a block back in true scale
+  auto store = [&](const double* src, int slot, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
-    for (int e = threadIdx.x; e < m * nc; e += nthr) {
-      const int c = e / m, r = e - c * m;
-      __stcg(P.X + (size_t)(c0 + c) * P.ldx + r, src[c * m + r]);
+    for (int c = warp; c < nc; c += nw) {
+      double* dst = P.X + (size_t)(c0 + c) * P.ldx;
+      const double d = scl[slot][c];
+      for (int r = lane; r < m; r += 32) __stcg(dst + r, src[c * MP + r] * d);
     }
   };
   auto ld_col = [&](double (&x)[RPL], const double* col) {
 #pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      x[i] = r < m ? col[r] : 0.0;
-    }
+    for (int i = 0; i < RPL; ++i) x[i] = col[lane + 32 * i];
   };
   auto st_col = [&](const double (&x)[RPL], double* col) {
 #pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      if (r < m) col[r] = x[i];
+    for (int i = 0; i < RPL; ++i) col[lane + 32 * i] = x[i];
+  };
+  auto get_st = [&](int slot, int c) { return ColSt{nrm[slot][c], scl[slot][c], iscl[slot][c]}; };
+  auto put_st = [&](int slot, int c, const ColSt& st) {
+    if (lane == 0) { nrm[slot][c] = st.n2; scl[slot][c] = st.d; iscl[slot][c] = st.id; }
+  };
+  // K = 2: both blocks' within-pairs of round r on one warp (two
+  // independent rotations per step), B/2 warps, named barrier 1
+  auto within2 = [&](bool& any) {
+    for (int r = 0; r < B - 1; ++r) {
+      int p, q;
+      match(r, warp, B, p, q);
+      double xp[RPL], xq[RPL], yp[RPL], yq[RPL];
+      ld_col(xp, S0 + p * MP);
+      ld_col(xq, S0 + q * MP);
+      ld_col(yp, S1 + p * MP);
+      ld_col(yq, S1 + q * MP);
+      ColSt A0 = get_st(0, p), B0 = get_st(0, q), A1 = get_st(1, p), B1 = get_st(1, q);
+      bool r0, r1;
+      rotate2<RPL>(xp, xq, yp, yq, A0, B0, A1, B1, tol, tiny2, r0, r1);
+      if (r0) {
+        st_col(xp, S0 + p * MP);
+        st_col(xq, S0 + q * MP);
+        put_st(0, p, A0);
+        put_st(0, q, B0);
+      }
+      if (r1) {
+        st_col(yp, S1 + p * MP);
+        st_col(yq, S1 + q * MP);
+        put_st(1, p, A1);
+        put_st(1, q, B1);
+      }
+      any |= r0 | r1;
+      named_bar(1, B * 16);
+    }
+  };
+  // K = 2 cross phase: warp w keeps columns 2w, 2w+1 of block I in registers
+  // and meets the J column pairs (2j, 2j+1), j = w, w+1, ... mod B/2: four
+  // rotations per step as two interleaved pairs, half the shared-memory
+  // column traffic per rotation of the K = 1 scheme
+  auto cross2 = [&](bool& any) {
+    const int H = B / 2, p0 = 2 * warp, p1 = p0 + 1;
+    double a0[RPL], a1[RPL], b0[RPL], b1[RPL];
+    ld_col(a0, S0 + p0 * MP);
+    ld_col(a1, S0 + p1 * MP);
+    ColSt A0 = get_st(0, p0), A1 = get_st(0, p1);
+    bool dirty = false;
+    int j = warp;
+    for (int st = 0; st < H; ++st, j = (j + 1 == H) ? 0 : j + 1) {
+      named_bar(15, H * 32);
+      const int q0 = 2 * j, q1 = q0 + 1;
+      ld_col(b0, S1 + q0 * MP);
+      ld_col(b1, S1 + q1 * MP);
+      ColSt B0 = get_st(1, q0), B1 = get_st(1, q1);
+      bool r00, r11, r01, r10;
+      rotate2<RPL>(a0, b0, a1, b1, A0, B0, A1, B1, tol, tiny2, r00, r11);
+      rotate2<RPL>(a0, b1, a1, b0, A0, B1, A1, B0, tol, tiny2, r01, r10);
+      if (r00 | r10) {
+        st_col(b0, S1 + q0 * MP);
+        put_st(1, q0, B0);
+      }
+      if (r11 | r01) {
+        st_col(b1, S1 + q1 * MP);
+        put_st(1, q1, B1);
+      }
+      dirty |= r00 | r11 | r01 | r10;
+    }
+    if (dirty) {
+      st_col(a0, S0 + p0 * MP);
+      st_col(a1, S0 + p1 * MP);
+      put_st(0, p0, A0);
+      put_st(0, p1, A1);
+      any = true;
     }
   };
   // all pairs inside one block: round-robin tournament among B/2 warps
   // (warps [base, base + B/2)), synchronised on their own named barrier
-  auto within = [&](double* S, double* nr, int nc, int base, int bar_id, bool& any) {
+  auto within = [&](double* S, int slot, int nc, int base, int bar_id, bool& any) {
     const int w = warp - base;
     for (int r = 0; r < B - 1; ++r) {
       int p, q;
       match(r, w, B, p, q);
       if (p < nc && q < nc) {
         double xa[RPL], xb[RPL];
-        ld_col(xa, S + p * m);
-        ld_col(xb, S + q * m);
-        double al = nr[p], be = nr[q];
-        if (rotate_regs<RPL>(xa, xb, al, be, tol, tiny2)) {
+        ld_col(xa, S + p * MP);
+        ld_col(xb, S + q * MP);
+        double al = nrm[slot][p], be = nrm[slot][q];
+        double dp = scl[slot][p], ip = iscl[slot][p], dq = scl[slot][q], iq = iscl[slot][q];
+        if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2)) {
           any = true;
-          st_col(xa, S + p * m);
-          st_col(xb, S + q * m);
-          if (lane == 0) { nr[p] = al; nr[q] = be; }
+          st_col(xa, S + p * MP);
+          st_col(xb, S + q * MP);
+          if (lane == 0) {
+            nrm[slot][p] = al; nrm[slot][q] = be;
+            scl[slot][p] = dp; iscl[slot][p] = ip; scl[slot][q] = dq; iscl[slot][q] = iq;
+          }
         }
       }
       named_bar(bar_id, B * 16);
     }
   };
 
+  // zero both staging buffers once: the padded rows m..MP-1 are never loaded
+  for (int e = threadIdx.x; e < 2 * B * MP; e += nthr) sm[e] = 0.0;
+  __syncthreads();
   long long c_load = 0, c_within = 0, c_cross = 0, c_store = 0, c_sync = 0, c_conv = 0;
-  long long tt = clock64();
-  auto tick = [&](long long& acc) { const long long now = clock64(); acc += now - tt; tt = now; };
+  long long tt = kClockProf ? clock64() : 0;
+  auto tick = [&](long long& acc) {
+    if (kClockProf) { const long long now = clock64(); acc += now - tt; tt = now; }
+  };
   if (s > 1) {
     for (sweeps = 1; sweeps <= max_sweeps; ++sweeps) {
       bool any = false;
@@ -242,52 +396,58 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
           if (realJ) load(S1, J);
           cp_wait();
           __syncthreads();
-          norms_of(S0, nrm[0]);
-          if (realJ) norms_of(S1, nrm[1]);
+          norms_of(S0, 0);
+          if (realJ) norms_of(S1, 1);
+          else if (threadIdx.x < 16) nrm[1][threadIdx.x] = 0.0;   // dummy block: nothing rotates
           __syncthreads();
           tick(c_load);
           const int ncI = min(B, s - I * B);
           const int ncJ = realJ ? min(B, s - J * B) : 0;
-          if (r == 0) {   // pairs inside blocks I and J, concurrently on two warp halves
-            if (warp < B / 2) within(S0, nrm[0], ncI, 0, 1, any);
-            else if (realJ && warp < B) within(S1, nrm[1], ncJ, B / 2, 2, any);
+          if (r == 0) {   // pairs inside blocks I and J
+            if (K == 2) {
+              within2(any);
+            } else {      // concurrently on two warp halves
+              if (warp < B / 2) within(S0, 0, ncI, 0, 1, any);
+              else if (realJ && warp < B) within(S1, 1, ncJ, B / 2, 2, any);
+            }
             __syncthreads();
           }
           tick(c_within);
-          if (realJ && warp < B) {
+          if (K == 2) {
+            if (realJ) cross2(any);
+          } else if (realJ && warp < B) {
             // warp w keeps column w of block I in registers and meets the J
             // columns in order w, w+1, ...; the cross warps meet at a named
             // barrier between rounds (measured 1.8x faster than per-column
             // spin flags, which steal issue slots)
             const int p = warp;
             double xa[RPL], xb[RPL];
-            ld_col(xa, S0 + p * m);
-            double al = nrm[0][p];
+            ld_col(xa, S0 + p * MP);
+            double al = nrm[0][p], dp = scl[0][p], ip = iscl[0][p];
             bool dirty = false;
-            for (int rr = 0; rr < B; ++rr) {
-              const int q = (p + rr) % B;
-              // column q was used in round rr-1 by warp p+1: wait on q's
-              // producer/consumer barrier (ids 1..B, two warps each)
-              if (kPipelined) { if (rr > 0) named_bar(1 + q, 64); } else { named_bar(15, B * 32); }
+            int q = p;
+            for (int rr = 0; rr < B; ++rr, q = (q + 1 == B) ? 0 : q + 1) {
+              named_bar(15, B * 32);
               if (p < ncI && q < ncJ) {
-                ld_col(xb, S1 + q * m);
-                double be = nrm[1][q];
-                if (rotate_regs<RPL>(xa, xb, al, be, tol, tiny2)) {
+                ld_col(xb, S1 + q * MP);
+                double be = nrm[1][q], dq = scl[1][q], iq = iscl[1][q];
+                if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2)) {
                   any = true;
                   dirty = true;
-                  st_col(xb, S1 + q * m);
-                  if (lane == 0) nrm[1][q] = be;
+                  st_col(xb, S1 + q * MP);
+                  if (lane == 0) { nrm[1][q] = be; scl[1][q] = dq; iscl[1][q] = iq; }
                 }
               }
-              // hand column q to warp p-1 (its round rr+1); bar.arrive orders the stores
-              if (kPipelined && rr < B - 1) named_arrive(1 + q, 64);
             }
-            if (dirty) st_col(xa, S0 + p * m);
+            if (dirty) {
+              st_col(xa, S0 + p * MP);
+              if (lane == 0) { scl[0][p] = dp; iscl[0][p] = ip; }
+            }
           }
           __syncthreads();
           tick(c_cross);
-          store(S0, I);
-          if (realJ) store(S1, J);
+          store(S0, 0, I);
+          if (realJ) store(S1, 1, J);
           __syncthreads();
           tick(c_store);
         }
@@ -377,8 +537,10 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
   if (probs.empty()) return;
   int mmax = 1;
   for (const JacobiProb& p : probs) mmax = std::max(mmax, p.m);
+  // staged column stride MP = 32 RPL of the instantiation chosen below
+  const int MP = mmax <= 512 ? 512 : mmax <= 768 ? 768 : mmax <= 1024 ? 1024 : 2048;
   int B = 16;
-  while (B > 2 && (size_t)2 * B * mmax * 8 > 200 * 1024) B >>= 1;
+  while (B > 2 && (size_t)2 * B * MP * 8 > 227 * 1024 - 1024) --B;
   // group by cluster size: one CTA per block pair of a round, at most 8
   static int max_g = [] {
     const char* e = getenv("TLRB_JACOBI_MAXCL");
@@ -443,12 +605,15 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     int Bg = (smax + 2 * CL - 1) / (2 * CL);
     Bg = std::min(B, std::max(2, (Bg + 1) & ~1));
     // rows per lane and the thread bound (registers: 2 RPL doubles per lane)
-    auto kern = mmax <= 512 ? jacobi_cluster_kernel<16, 512>
-              : mmax <= 768 ? jacobi_cluster_kernel<24, 512>
-              : mmax <= 1024 ? jacobi_cluster_kernel<32, 256> : jacobi_cluster_kernel<64, 128>;
+    // K = 2 (two register columns per warp, B/2 warps) where the registers
+    // allow it; one column per warp for the long columns
+    auto kern = mmax <= 512 ? jacobi_cluster_kernel<16, 256, 2>
+              : mmax <= 768 ? jacobi_cluster_kernel<24, 256, 2>
+              : mmax <= 1024 ? jacobi_cluster_kernel<32, 256, 1> : jacobi_cluster_kernel<64, 128, 1>;
+    const int K = mmax <= 768 ? 2 : 1;
     const int bmax = mmax <= 768 ? 14 : mmax <= 1024 ? 8 : 4;
     if (Bg > bmax) Bg = bmax;
-    const size_t smem = std::max((size_t)2 * Bg * mmax * 8, (size_t)smax * 12 + 64);
+    const size_t smem = std::max((size_t)2 * Bg * MP * 8, (size_t)smax * 12 + 64);
     TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     double by = 0;
@@ -457,7 +622,7 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
       ProfScope ps(K_JACOBI, st, 0, by);  // flops added once the sweep counts are known
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(groups[g].size() * CL));
-      cfg.blockDim = dim3(32 * Bg);
+      cfg.blockDim = dim3(32 * Bg / K);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];

@@ -3,6 +3,8 @@
 // log-determinant and dot-product reductions, compression bookkeeping.
 #include "common.cuh"
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 namespace tlrb {
 
@@ -31,23 +33,33 @@ void Profiler::end(cudaStream_t s, double fl, double by) {
   if (open_cls < 0) return;
   cudaEvent_t b = get();
   TLRB_CUDA(cudaEventRecord(b, s));
-  pend.push_back({open_cls, open_ev, b});
+  pend.push_back({open_cls, open_ev, b, s});
   flops[open_cls] += fl;
   bytes[open_cls] += by;
   count[open_cls] += 1;
   open_cls = -1;
 }
 void Profiler::drain() {
+  static const char* tl_path = getenv("TLRB_TIMELINE");
+  FILE* tl = (tl_path && epoch) ? fopen(tl_path, "a") : nullptr;
   for (const Pend& p : pend) {
     float a = 0;
     if (cudaEventElapsedTime(&a, p.a, p.b) == cudaSuccess) ms[p.cls] += a;
+    float t0 = 0;
+    if (tl && cudaEventElapsedTime(&t0, epoch, p.a) == cudaSuccess)
+      fprintf(tl, "%s %.4f %.4f %p\n", kclass_name[p.cls], t0, t0 + a, (void*)p.s);
     pool.push_back(p.a);
     pool.push_back(p.b);
   }
   pend.clear();
+  if (tl) fclose(tl);
 }
 void Profiler::reset() {
   drain();
+  if (getenv("TLRB_TIMELINE")) {   // new time origin
+    if (!epoch) TLRB_CUDA(cudaEventCreate(&epoch));
+    TLRB_CUDA(cudaEventRecord(epoch, 0));
+  }
   for (int i = 0; i < K_NCLASS; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0;
 }
 

@@ -297,8 +297,10 @@ __global__ void __launch_bounds__(NT) qrcp_cluster_kernel(const QrcpProb* __rest
     }
   };
   long long c_cand = 0, c_fetch = 0, c_refl = 0, c_upd = 0, c_pub = 0, c_sync = 0;
-  long long tt = clock64();
-  auto tick = [&](long long& a) { const long long nw_ = clock64(); a += nw_ - tt; tt = nw_; };
+  long long tt = kClockProf ? clock64() : 0;
+  auto tick = [&](long long& a) {
+    if (kClockProf) { const long long nw_ = clock64(); a += nw_ - tt; tt = nw_; }
+  };
   for (; j < kmax; ++j) {
     const int par = j & 1;
     if (warp == 0) {
@@ -537,6 +539,30 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   for (size_t i = 0; i < probs.size(); ++i) {
     if (cluster_ok && probs[i].hint > thr) { big.push_back(probs[i]); big_idx.push_back((int)i); }
     else small.push_back(probs[i]);
+  }
+  // large problems: blocked randomized QRCP (bqrcp.cu), GEMM-based and not
+  // bound by cluster occupancy; TLRB_QRCP_BLOCKED=<min batch> (0 = never)
+  // The cluster kernel has the lower latency for a lone matrix, the blocked
+  // one the higher throughput: it is used once the big problems exceed the
+  // clusters that can be co-resident (7 of 16 CTAs on 148 SMs).
+  static const int blocked_min = getenv("TLRB_QRCP_BLOCKED") ? atoi(getenv("TLRB_QRCP_BLOCKED")) : 8;
+  if (blocked_min > 0 && (int)big.size() >= blocked_min && mmax <= 2048 && nmax <= 2048) {
+    const QrcpLaunch Ls = stage(small, ar, s);
+    if (!Ls.count) { launch_qrcp_blocked(big, ar, s); return; }
+    static cudaStream_t side2 = nullptr;
+    static cudaEvent_t f2 = nullptr, j2 = nullptr;
+    if (!side2) {
+      TLRB_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+      TLRB_CUDA(cudaEventCreateWithFlags(&f2, cudaEventDisableTiming));
+      TLRB_CUDA(cudaEventCreateWithFlags(&j2, cudaEventDisableTiming));
+    }
+    TLRB_CUDA(cudaEventRecord(f2, s));
+    TLRB_CUDA(cudaStreamWaitEvent(side2, f2, 0));
+    run_single(Ls, side2);
+    launch_qrcp_blocked(big, ar, s);
+    TLRB_CUDA(cudaEventRecord(j2, side2));
+    TLRB_CUDA(cudaStreamWaitEvent(s, j2, 0));
+    return;
   }
   const QrcpLaunch Lb = stage(big, ar, s), Ls = stage(small, ar, s);
   if (!Lb.count) { run_single(Ls, s); return; }

@@ -34,8 +34,14 @@ using namespace tlrb;
 
 namespace {
 
-// truncated QRCP stops at ||residual||_F <= 1e-3 acc ||M||_F
-constexpr double kQrcpRelTol = 1e-3;
+// truncated QRCP stops at ||residual||_F <= rel acc ||M||_F.  The residual
+// enters the truncation tail exactly; the top-k sigma(R) differ from sigma(M)
+// by at most rel^2 acc^2 ||M||^2 in the squared tail sums, i.e. rel^2 of the
+// truncation threshold.  TLRB_QRCP_REL overrides.
+double qrcp_rel_tol() {
+  static const double v = getenv("TLRB_QRCP_REL") ? atof(getenv("TLRB_QRCP_REL")) : 1e-2;
+  return v;
+}
 constexpr int kPotrfBlock = 32;
 
 struct Flops {
@@ -248,7 +254,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
       Job& J = jobs[j];
       cp.push_back({J.M, J.m, J.E, J.m, J.m, J.n, 0, 1.0, 0, nullptr});
       qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, h->d_rank + j, h->d_sums + 6 * j + 1,
-                    (kQrcpRelTol * acc) * (kQrcpRelTol * acc), J.s});
+                    (qrcp_rel_tol() * acc) * (qrcp_rel_tol() * acc), J.s});
     }
     launch_copy(cp, h->ar, s);
     launch_qrcp(qp, gathered, h->ar, s);

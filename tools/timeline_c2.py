@@ -1,0 +1,66 @@
+"""Kernel timeline of one warm C2 TLR evaluation (TLRB_TIMELINE dump of the
+per-launch CUDA events): busy/idle time, per-class union, 10 ms buckets.
+    python tools/timeline_c2.py [acc]"""
+import os
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+path = os.path.join(tempfile.gettempdir(), "tlrb_timeline.txt")
+os.environ["TLRB_TIMELINE"] = path
+import paper_1804_09137_b200 as tb  # noqa: E402
+from paper_1804_09137_b200 import _lib  # noqa: E402
+
+acc = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-9
+locs = tb.generate_locations(10000, 0)
+z = np.load(ROOT / "tests/golden/z_big.npz")["C2"]
+h = tb.Handle(locs.coords, 500)
+p = tb.MaternParams(1.0, 0.1, 0.5)
+h.loglik(z, p, acc)
+if os.path.exists(path):
+    os.remove(path)
+_lib.profile_enable(True)
+h.loglik(z, p, acc)
+_lib.profile_read()
+rows = [ln.split() for ln in open(path)]
+ev = sorted((float(a), float(b), c) for c, a, b, _ in rows)
+t0 = ev[0][0]
+end = max(b for _, b, _ in ev)
+
+
+def union(iv):
+    tot, cur_a, cur_b = 0.0, None, None
+    for a, b in sorted(iv):
+        if cur_b is None or a > cur_b:
+            if cur_b is not None:
+                tot += cur_b - cur_a
+            cur_a, cur_b = a, b
+        else:
+            cur_b = max(cur_b, b)
+    if cur_b is not None:
+        tot += cur_b - cur_a
+    return tot
+
+
+busy = union([(a, b) for a, b, _ in ev])
+print(f"span {end - t0:.1f} ms  busy(any kernel) {busy:.1f} ms  idle {end - t0 - busy:.1f} ms  launches {len(ev)}")
+for c in sorted({c for _, _, c in ev}):
+    iv = [(a, b) for a, b, cc in ev if cc == c]
+    print(f"  {c:16s} union {union(iv):8.1f} ms  sum {sum(b - a for a, b in iv):8.1f} ms  n {len(iv)}")
+# 10 ms buckets: fraction of time each class is active
+B = 10.0
+nb = int((end - t0) / B) + 1
+cls = sorted({c for _, _, c in ev})
+print("bucket(ms) " + " ".join(f"{c[:6]:>6s}" for c in cls) + "  idle")
+for k in range(nb):
+    lo, hi = t0 + k * B, t0 + (k + 1) * B
+    fr = []
+    for c in cls:
+        iv = [(max(a, lo), min(b, hi)) for a, b, cc in ev if cc == c and b > lo and a < hi]
+        fr.append(union(iv) / B)
+    anyiv = [(max(a, lo), min(b, hi)) for a, b, _ in ev if b > lo and a < hi]
+    print(f"{k * B:8.0f}   " + " ".join(f"{f:6.2f}" for f in fr) + f"  {1 - union(anyiv) / B:5.2f}")
