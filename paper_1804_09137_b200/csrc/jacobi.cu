@@ -81,7 +81,7 @@ __device__ __forceinline__ double fast_rcp(double x) {
 template <int RPL>
 __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL], double& al, double& be,
                                             double& dp, double& ip, double& dq, double& iq, double tol,
-                                            double tiny2) {
+                                            double tiny2, double d2, bool& big) {
   if (al <= tiny2 || be <= tiny2) return false;
   double g0 = 0.0, g1 = 0.0;
 #pragma unroll
@@ -91,6 +91,7 @@ __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL]
   }
   const double ga = wsum(g0 + g1) * (dp * dq);
   if (ga == 0.0 || ga * ga <= (tol * tol) * (al * be)) return false;
+  big |= ga * ga > d2 * (al * be);
   // t = sign(zeta)/(|zeta| + sqrt(1+zeta^2)), zeta = (be-al)/(2ga), written
   // with one reciprocal: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)).  The
   // rotation only has to be orthogonal to ~u, so hardware rsqrt / rcp seeds
@@ -126,7 +127,7 @@ struct ColSt {
 template <int RPL>
 __device__ __forceinline__ void rotate2(double (&a0)[RPL], double (&b0)[RPL], double (&a1)[RPL], double (&b1)[RPL],
                                         ColSt& A0, ColSt& B0, ColSt& A1, ColSt& B1, double tol, double tiny2,
-                                        bool& r0, bool& r1) {
+                                        double d2, bool& big, bool& r0, bool& r1) {
   double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
 #pragma unroll
   for (int i = 0; i < RPL; i += 2) {
@@ -147,6 +148,7 @@ __device__ __forceinline__ void rotate2(double (&a0)[RPL], double (&b0)[RPL], do
   const double tol2 = tol * tol;
   r0 = A0.n2 > tiny2 && B0.n2 > tiny2 && ga0 != 0.0 && ga0 * ga0 > tol2 * (A0.n2 * B0.n2);
   r1 = A1.n2 > tiny2 && B1.n2 > tiny2 && ga1 != 0.0 && ga1 * ga1 > tol2 * (A1.n2 * B1.n2);
+  big |= (r0 && ga0 * ga0 > d2 * (A0.n2 * B0.n2)) || (r1 && ga1 * ga1 > d2 * (A1.n2 * B1.n2));
   // t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)), d = beta - alpha, g2 = 2 gamma
   const double d0 = B0.n2 - A0.n2, d1 = B1.n2 - A1.n2;
   const double e0 = 2.0 * ga0, e1 = 2.0 * ga1;
@@ -180,6 +182,8 @@ __device__ __forceinline__ void rotate2(double (&a0)[RPL], double (&b0)[RPL], do
   }
 }
 
+__constant__ int c_early_exit = 1;
+
 template <int RPL, int NT, int K>
 __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
                                                              int max_sweeps) {
@@ -206,6 +210,12 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   const double tol = fmin((double)m * DBL_EPSILON, fmax(0.01 * P.eps, 2.0 * sqrt((double)m) * DBL_EPSILON));
   const double tau = fmax(1e-3 * P.eps, 2.0 * sqrt((double)m) * DBL_EPSILON);
   const double tiny2 = tau * tau * P.aux[2];
+  // Early exit: cyclic Jacobi converges quadratically at the end, so once no
+  // pair of a sweep had |cos| above delta = sqrt(0.1 tol), the next sweep
+  // could only meet cosines ~delta^2 < tol and would rotate nothing: the
+  // sweep loop stops without that (otherwise rotation-free) check sweep.
+  // `any` below means "some pair above delta"; TLRB_JACOBI_EARLY=0 -> delta = tol.
+  const double d2 = c_early_exit ? 0.1 * tol : tol * tol;
   const int nblk = (s + B - 1) / B;
   const int np = nblk + (nblk & 1);   // pad with a dummy block
   int sweeps = 0;
@@ -291,7 +301,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
       ld_col(yq, S1 + q * MP);
       ColSt A0 = get_st(0, p), B0 = get_st(0, q), A1 = get_st(1, p), B1 = get_st(1, q);
       bool r0, r1;
-      rotate2<RPL>(xp, xq, yp, yq, A0, B0, A1, B1, tol, tiny2, r0, r1);
+      rotate2<RPL>(xp, xq, yp, yq, A0, B0, A1, B1, tol, tiny2, d2, any, r0, r1);
       if (r0) {
         st_col(xp, S0 + p * MP);
         st_col(xq, S0 + q * MP);
@@ -304,7 +314,6 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
         put_st(1, p, A1);
         put_st(1, q, B1);
       }
-      any |= r0 | r1;
       named_bar(1, B * 16);
     }
   };
@@ -327,8 +336,8 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
       ld_col(b1, S1 + q1 * MP);
       ColSt B0 = get_st(1, q0), B1 = get_st(1, q1);
       bool r00, r11, r01, r10;
-      rotate2<RPL>(a0, b0, a1, b1, A0, B0, A1, B1, tol, tiny2, r00, r11);
-      rotate2<RPL>(a0, b1, a1, b0, A0, B1, A1, B0, tol, tiny2, r01, r10);
+      rotate2<RPL>(a0, b0, a1, b1, A0, B0, A1, B1, tol, tiny2, d2, any, r00, r11);
+      rotate2<RPL>(a0, b1, a1, b0, A0, B1, A1, B0, tol, tiny2, d2, any, r01, r10);
       if (r00 | r10) {
         st_col(b0, S1 + q0 * MP);
         put_st(1, q0, B0);
@@ -344,7 +353,6 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
       st_col(a1, S0 + p1 * MP);
       put_st(0, p0, A0);
       put_st(0, p1, A1);
-      any = true;
     }
   };
   // all pairs inside one block: round-robin tournament among B/2 warps
@@ -360,8 +368,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
         ld_col(xb, S + q * MP);
         double al = nrm[slot][p], be = nrm[slot][q];
         double dp = scl[slot][p], ip = iscl[slot][p], dq = scl[slot][q], iq = iscl[slot][q];
-        if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2)) {
-          any = true;
+        if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2, d2, any)) {
           st_col(xa, S + p * MP);
           st_col(xb, S + q * MP);
           if (lane == 0) {
@@ -431,8 +438,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
               if (p < ncI && q < ncJ) {
                 ld_col(xb, S1 + q * MP);
                 double be = nrm[1][q], dq = scl[1][q], iq = iscl[1][q];
-                if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2)) {
-                  any = true;
+                if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2, d2, any)) {
                   dirty = true;
                   st_col(xb, S1 + q * MP);
                   if (lane == 0) { nrm[1][q] = be; scl[1][q] = dq; iscl[1][q] = iq; }
@@ -535,6 +541,15 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
 
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
+  static const bool early_set = [] {
+    const char* e = getenv("TLRB_JACOBI_EARLY");
+    if (e && atoi(e) == 0) {
+      const int off = 0;
+      TLRB_CUDA(cudaMemcpyToSymbol(c_early_exit, &off, sizeof off));
+    }
+    return true;
+  }();
+  (void)early_set;
   int mmax = 1;
   for (const JacobiProb& p : probs) mmax = std::max(mmax, p.m);
   // staged column stride MP = 32 RPL of the instantiation chosen below
