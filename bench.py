@@ -348,11 +348,16 @@ def main():
                                   "max_rank": h.last_stats["max_rank"]}
         line["variants"] = var
     if not args.no_cpu:
-        from oracle import cpu_baseline as cb
-        from oracle import tlr_oracle as orc
-        est, desc = cb.estimate_eval_seconds(orc.generate_locations(N_POINTS, 0), z, THETA, NB, args.acc)
-        line["cpu_baseline"] = {"value": est, "unit": "s", "cores": cb.host_threads(), "kind": "port",
-                                "sample": desc}
+        # in a fresh interpreter (no torch / CUDA runtime threads next to the
+        # BLAS pool), the same way the --impl reference arm runs
+        code = ("import json, sys; sys.path.insert(0, %r); import bench; "
+                "from oracle import cpu_baseline as cb; from oracle import tlr_oracle as orc; "
+                "est, desc = cb.estimate_eval_seconds(orc.generate_locations(bench.N_POINTS, 0), bench.load_z(), "
+                "bench.THETA, bench.NB, %r); print(json.dumps([est, desc, cb.host_threads()]))"
+                % (str(Path(__file__).resolve().parent), args.acc))
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True)
+        est, desc, cores = json.loads(out.stdout.strip().splitlines()[-1])
+        line["cpu_baseline"] = {"value": est, "unit": "s", "cores": cores, "kind": "port", "sample": desc}
     print(json.dumps(line))
     if world > 1:
         dist.barrier()
