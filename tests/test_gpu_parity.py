@@ -311,3 +311,64 @@ def test_c3_full_dense_parity(tb):
     llt = tb.log_likelihood(locs, z, tb.MaternParams(*e["theta"]),
                             tb.LikelihoodConfig(mode="tlr", accuracy=1e-7, nb=e["nb"], max_rank=380))
     assert abs(llt - ref) <= 10 * 1e-7 * abs(ref)
+
+
+_BLOCKED_SCRIPT = r"""
+import sys, json
+import numpy as np
+sys.path.insert(0, %r)
+import paper_1804_09137_b200 as tb
+g = np.load(%r)
+out = {}
+for i, j in [(1, 0), (2, 0), (3, 0), (3, 2)]:
+    tile = g[f"tile_{i}_{j}"]
+    nrm = np.linalg.norm(tile)
+    for eps in (1e-5, 1e-7, 1e-9, 1e-12):
+        u, v = tb.compress_tile(tile, eps)
+        out[f"{i}_{j}_{eps:g}"] = [int(u.shape[1]), float(np.linalg.norm(tile - u @ v.T) / nrm)]
+print(json.dumps(out))
+"""
+
+
+def test_compress_ranks_blocked_qrcp(tb):
+    """The blocked randomized QRCP (bqrcp.cu; forced for single problems with
+    TLRB_QRCP_BLOCKED=1 in a child process) gives the reference ranks and
+    the accuracy bound on the golden tiles, like the cluster kernel."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    code = _BLOCKED_SCRIPT % (str(ROOT), str(GOLD / "compression.npz"))
+    env = dict(os.environ, TLRB_QRCP_BLOCKED="1", TLRB_QRCP_CLUSTER_MIN="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    g = np.load(GOLD / "compression.npz")
+    for key, (rank, rel) in out.items():
+        i, j, eps = key.split("_")
+        assert rank == int(g[f"rank_{i}_{j}_{eps}"]), (key, rank)
+        assert rel <= float(eps) * (1 + 1e-6), (key, rel)
+
+
+def test_loglik_blocked_qrcp_everywhere(tb, gold):
+    """C1 with every compression batch on the blocked QRCP (child process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    code = (f"import sys, json, numpy as np; sys.path.insert(0, {str(ROOT)!r}); "
+            "import paper_1804_09137_b200 as tb; "
+            f"z = np.load({str(GOLD / 'z_big.npz')!r})['C1']; "
+            "locs = tb.generate_locations(1600, 0); "
+            "cfg = tb.LikelihoodConfig(mode='tlr', accuracy=1e-9, nb=400); "
+            "print(json.dumps(tb.log_likelihood(locs, z, tb.MaternParams(1.0, 0.1, 0.5), cfg)))")
+    env = dict(os.environ, TLRB_QRCP_BLOCKED="1", TLRB_QRCP_CLUSTER_MIN="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    ll = json.loads(res.stdout.strip().splitlines()[-1])
+    ref = gold["loglik"]["C1"]["modes"]["tlr:1e-09"]["ll"]
+    assert abs(ll - ref) <= 1e-8 * abs(ref), (ll, ref)
