@@ -237,10 +237,18 @@ def main():
         torch.cuda.synchronize()
         return h.loglik_device(dz.data_ptr(), p, acc)
 
-    for _ in range(args.warmup):
+    for _ in range(max(0, args.warmup - 1)):
         one(args.acc)
-    barrier()
+    # last warm-up step: every kernel class under per-launch CUDA events ->
+    # the per-class breakdown and the dominant class (outside the timed region)
     _lib.profile_enable(True)
+    one(args.acc)
+    barrier()
+    prof_all = _lib.profile_read()
+    dom_name = max(prof_all.items(), key=lambda kv: kv[1]["ms"])[0]
+    # timed region: events only around the dominant class's launches (a few
+    # dozen per step), so the roofline is measured live at ~zero overhead
+    _lib.profile_enable(True, classes=[dom_name])
     l0 = tb.launch_count()
     step_ms, lls, stats = [], [], []
     with ClockSampler(local) as clk:
@@ -279,9 +287,8 @@ def main():
 
     peaks = measured_peaks()
     p64 = fp64_peak_tflops(torch)
-    # dominant kernel class by device time inside the timed region
-    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
-    name, d = dom
+    # dominant kernel class (from the all-class warm-up step), timed inside the timed region
+    name, d = dom_name, prof[dom_name]
     per_launch_s = d["ms"] * 1e-3 / max(1, d["launches"])
     flops_bound = d["flops"] > 0 and (d["flops"] / (p64 * 1e12)) >= (d["bytes"] / (peaks["hbm_gbs"] * 1e9))
     if flops_bound:
@@ -295,11 +302,13 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("fallback") else "")}
     roof["kernel"] = name
     roof["share_of_step"] = d["ms"] / (ms * args.steps)
+    roof["note"] = ("dominant class timed with per-launch CUDA events inside the timed region; "
+                    "algorithmic flops per SURVEY 8(d) / as implemented (Jacobi: 3 n s(s-1) per sweep)")
     roof["launches_per_step"] = d["launches"] / args.steps
     roof["traffic"] = traffic_for(name)
-    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                   "gflop_per_step": v["flops"] / args.steps / 1e9, "gb_per_step": v["bytes"] / args.steps / 1e9}
-               for k, v in prof.items() if v["launches"]}
+    kernels = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"],
+                   "gflop_per_step": v["flops"] / 1e9, "gb_per_step": v["bytes"] / 1e9}
+               for k, v in prof_all.items() if v["launches"]}   # one profiled warm-up step
     st = stats[-1]
     ref = REF_LL.get(ref_key(args.acc))
     line = {

@@ -155,6 +155,9 @@ int64_t tlrb_launch_count(void);
  * plus the algorithmic flops / bytes of each launch.
  * enable resets the counters.  Classes: 0..10 (name returned). */
 int32_t tlrb_profile_enable(int32_t on);
+/* Restrict the profiler to the classes whose bit is set (default: all), so a
+ * timed region can carry events for one kernel class only. */
+int32_t tlrb_profile_mask(uint32_t mask);
 int32_t tlrb_profile_read(int32_t cls, char* name, int32_t len, double* ms, double* flops,
                           double* bytes, int64_t* launches);
 

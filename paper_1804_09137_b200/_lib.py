@@ -71,6 +71,7 @@ SIGNATURES = [
     ("tlrb_compress_tile", C.c_int32, [_DP, C.c_int32, C.c_int32, C.c_double, _IP, _DP, _DP, C.c_int32]),
     ("tlrb_launch_count", C.c_int64, []),
     ("tlrb_profile_enable", C.c_int32, [C.c_int32]),
+    ("tlrb_profile_mask", C.c_int32, [C.c_uint32]),
     ("tlrb_profile_read", C.c_int32, [C.c_int32, C.c_char_p, C.c_int32, _DP, _DP, _DP,
                                       C.POINTER(C.c_int64)]),
 ]
@@ -94,8 +95,17 @@ def load():
     return lib
 
 
-def profile_enable(on: bool = True):
-    load().tlrb_profile_enable(1 if on else 0)
+KERNEL_CLASSES = ("gen_tiles", "dgemm_vbatch", "trsm_vbatch", "potrf_block", "qr_householder",
+                  "jacobi_svd", "sumsq", "copy", "unused", "reduce", "cross_gemv")
+
+
+def profile_enable(on: bool = True, classes=None):
+    """Reset and (de)activate the per-launch CUDA-event profiler; `classes`
+    (names) restricts it to those kernel classes."""
+    lib = load()
+    mask = 0xFFFFFFFF if classes is None else sum(1 << KERNEL_CLASSES.index(c) for c in classes)
+    lib.tlrb_profile_mask(mask)
+    lib.tlrb_profile_enable(1 if on else 0)
 
 
 def profile_read() -> dict:

@@ -38,6 +38,7 @@ enum KClass { K_GEN = 0, K_GEMM, K_TRSM, K_POTRF, K_QR, K_JACOBI, K_SUMSQ, K_COP
 extern const char* kclass_name[K_NCLASS];
 struct Profiler {
   bool on = false;
+  unsigned mask = ~0u;   // kernel classes timed while on (tlrb_profile_mask)
   double ms[K_NCLASS] = {}, flops[K_NCLASS] = {}, bytes[K_NCLASS] = {};
   int64_t count[K_NCLASS] = {};
   struct Pend { int cls; cudaEvent_t a, b; cudaStream_t s; };
@@ -49,17 +50,20 @@ struct Profiler {
   cudaEvent_t get();
   void begin(int cls, cudaStream_t s);
   void end(cudaStream_t s, double fl, double by);
-  void add_work(int cls, double fl, double by) { flops[cls] += fl; bytes[cls] += by; }
+  void add_work(int cls, double fl, double by) {
+    if ((mask >> cls) & 1u) { flops[cls] += fl; bytes[cls] += by; }
+  }
   void drain();   // after a stream synchronisation
   void reset();
 };
 extern Profiler g_prof;
 struct ProfScope {   // RAII: times one launch of class cls
-  cudaStream_t s; double fl, by;
-  ProfScope(int cls, cudaStream_t st, double f = 0, double b = 0) : s(st), fl(f), by(b) {
-    if (g_prof.on) g_prof.begin(cls, st);
+  cudaStream_t s; double fl, by; bool act;
+  ProfScope(int cls, cudaStream_t st, double f = 0, double b = 0)
+      : s(st), fl(f), by(b), act(g_prof.on && ((g_prof.mask >> cls) & 1u)) {
+    if (act) g_prof.begin(cls, st);
   }
-  ~ProfScope() { if (g_prof.on) g_prof.end(s, fl, by); }
+  ~ProfScope() { if (act) g_prof.end(s, fl, by); }
 };
 
 // clock64 phase counters inside the QRCP / Jacobi kernels (TLRB_QRCP_PROF /

@@ -323,8 +323,9 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     Job& J = jobs[j];
     J.out_rank = J.s ? rk[j] : 0;
     h->max_sweeps = std::max(h->max_sweeps, J.s ? sw[j] : 0);
-    // one-sided Jacobi: per sweep s(s-1)/2 pairs x (3 dots + rotation) = 12 n flops each
-    if (g_prof.on && J.s) g_prof.add_work(K_JACOBI, 6.0 * J.n * (double)J.s * (J.s - 1) * sw[j], 0);
+    // one-sided Jacobi as implemented: per sweep s(s-1)/2 pairs x (one dot,
+    // 2n flops, + the scaled rotation, 4n flops) = 3 n s (s-1) flops
+    if (g_prof.on && J.s) g_prof.add_work(K_JACOBI, 3.0 * J.n * (double)J.s * (J.s - 1) * sw[j], 0);
     const int k = J.out_rank;
     J.dense_out = h->max_rank > 0 && k > h->max_rank && !J.factored;
     if (J.tile >= 0) {   // the destination tile's storage is sized by the new rank
@@ -1479,6 +1480,11 @@ int64_t tlrb_launch_count(void) { return g_launches; }
 int32_t tlrb_profile_enable(int32_t on) {
   g_prof.reset();
   g_prof.on = on != 0;
+  return TLRB_OK;
+}
+
+int32_t tlrb_profile_mask(uint32_t mask) {
+  g_prof.mask = mask;
   return TLRB_OK;
 }
 
