@@ -115,6 +115,39 @@ __device__ __forceinline__ bool rotate_regs(double (&xa)[RPL], double (&xb)[RPL]
   return true;
 }
 
+// ---- 1-D bulk copies (TMA engine) between global memory and shared memory
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
 // Column state of a staged column: true squared norm, scale, 1/scale.
 struct ColSt {
   double n2, d, id;
@@ -185,7 +218,7 @@ __device__ __forceinline__ void rotate2(double (&a0)[RPL], double (&b0)[RPL], do
 __constant__ int c_early_exit = 1;
 
 template <int RPL, int NT, int K>
-__global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
+__global__ void __launch_bounds__(NT, 1) jacobi_cluster_kernel(const JacobiProb* __restrict__ probs, int B,
                                                              int max_sweeps) {
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -203,8 +236,11 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   __shared__ double nrm[2][16];      // maintained true squared column norms of S0 / S1
   __shared__ double scl[2][16], iscl[2][16];   // column scales (true column = scl * stored)
   __shared__ int rot_flag;
+  __shared__ alignas(8) unsigned long long ld_bar;   // bulk-load completion (tx bytes)
+  __shared__ int dirt[2][16];                        // column rotated since its load
   // rotation tolerance: LAPACK dgesvj's m*eps, tightened for very small acc
-  // (the truncated product M V V^T inherits the columns' non-orthogonality);
+  // (the truncated product M V V^T inherits the columns' non-orthogonality;
+  // a looser 0.01 acc was measured to move the C2 likelihood by 1e-10 rel.);
   // columns below tau*||M|| carry no information for the truncation at acc
   // (their energy is preserved by the rotations) and are not rotated.
   const double tol = fmin((double)m * DBL_EPSILON, fmax(0.01 * P.eps, 2.0 * sqrt((double)m) * DBL_EPSILON));
@@ -224,6 +260,9 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   // columns are 16-byte aligned, so every load of the block is in flight at
   // once; completed by cp_wait() before the next barrier
   const bool vec = ((m & 1) == 0) && ((P.ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.X) & 15) == 0);
+  const bool bulk = vec;   // 16-byte aligned columns of m*8 bytes: TMA bulk copies
+  unsigned ld_phase = 0;
+  if (threadIdx.x == 0) mbar_init(&ld_bar, 1);
   auto load = [&](double* dst, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     if (vec) {
@@ -250,30 +289,43 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   auto cp_wait = [&]() {
     if (vec) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   };
-  // true squared norms of a freshly loaded block (scales reset to 1)
-  auto norms_of = [&](const double* src, int slot) {
+  // Columns live in global memory in scaled form: true column c = d_c * X(:, c)
+  // with d_c in P.sigma[c] (1 at start; the epilogue turns it into sigma).
+  // On load: true squared norms and the scales of the block; a scale that has
+  // drifted far from 1 (products of cosines) is folded into the column.
+  auto norms_of = [&](double* src, int slot, int blk) {
+    const int c0 = blk * B, nc = min(B, s - c0);
     for (int c = warp; c < B; c += nw) {
+      double d = c < nc ? __ldcg(P.sigma + c0 + c) : 1.0;
+      const bool fold = d < 1e-100 || d > 1e100;
       double a0 = 0.0, a1 = 0.0;
 #pragma unroll
       for (int i = 0; i < RPL; i += 2) {
-        const double x0 = src[c * MP + lane + 32 * i];
+        double x0 = src[c * MP + lane + 32 * i];
+        if (fold) { x0 *= d; src[c * MP + lane + 32 * i] = x0; }
         a0 = fma(x0, x0, a0);
         if (i + 1 < RPL) {
-          const double x1 = src[c * MP + lane + 32 * (i + 1)];
+          double x1 = src[c * MP + lane + 32 * (i + 1)];
+          if (fold) { x1 *= d; src[c * MP + lane + 32 * (i + 1)] = x1; }
           a1 = fma(x1, x1, a1);
         }
       }
-      const double a = wsum(a0 + a1);
-      if (lane == 0) { nrm[slot][c] = a; scl[slot][c] = 1.0; iscl[slot][c] = 1.0; }
+      if (fold) d = 1.0;
+      const double a = wsum(a0 + a1) * (d * d);
+      if (lane == 0) {
+        nrm[slot][c] = a; scl[slot][c] = d; iscl[slot][c] = 1.0 / d;
+        if (fold) dirt[slot][c] = 1;
+      }
     }
   };
-  // write a block back in true scale
+  // write a block back (scaled form) with its scales
   auto store = [&](const double* src, int slot, int blk) {
     const int c0 = blk * B, nc = min(B, s - c0);
     for (int c = warp; c < nc; c += nw) {
+      if (!dirt[slot][c]) continue;
       double* dst = P.X + (size_t)(c0 + c) * P.ldx;
-      const double d = scl[slot][c];
-      for (int r = lane; r < m; r += 32) __stcg(dst + r, src[c * MP + r] * d);
+      for (int r = lane; r < m; r += 32) __stcg(dst + r, src[c * MP + r]);
+      if (lane == 0) P.sigma[c0 + c] = scl[slot][c];
     }
   };
   auto ld_col = [&](double (&x)[RPL], const double* col) {
@@ -286,7 +338,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   };
   auto get_st = [&](int slot, int c) { return ColSt{nrm[slot][c], scl[slot][c], iscl[slot][c]}; };
   auto put_st = [&](int slot, int c, const ColSt& st) {
-    if (lane == 0) { nrm[slot][c] = st.n2; scl[slot][c] = st.d; iscl[slot][c] = st.id; }
+    if (lane == 0) { nrm[slot][c] = st.n2; scl[slot][c] = st.d; iscl[slot][c] = st.id; dirt[slot][c] = 1; }
   };
   // K = 2: both blocks' within-pairs of round r on one warp (two
   // independent rotations per step), B/2 warps, named barrier 1
@@ -374,6 +426,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
           if (lane == 0) {
             nrm[slot][p] = al; nrm[slot][q] = be;
             scl[slot][p] = dp; iscl[slot][p] = ip; scl[slot][q] = dq; iscl[slot][q] = iq;
+            dirt[slot][p] = 1; dirt[slot][q] = 1;
           }
         }
       }
@@ -383,7 +436,11 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
 
   // zero both staging buffers once: the padded rows m..MP-1 are never loaded
   for (int e = threadIdx.x; e < 2 * B * MP; e += nthr) sm[e] = 0.0;
-  __syncthreads();
+  // column scales start at 1 (every CTA writes the same values; the cluster
+  // barrier orders them before any CTA's first store of a rotated scale)
+  for (int c = threadIdx.x; c < s; c += nthr) P.sigma[c] = 1.0;
+  __threadfence();
+  cl.sync();
   long long c_load = 0, c_within = 0, c_cross = 0, c_store = 0, c_sync = 0, c_conv = 0;
   long long tt = kClockProf ? clock64() : 0;
   auto tick = [&](long long& acc) {
@@ -399,12 +456,32 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
           match(r, idx, np, I, J);
           if (I >= nblk) { const int t = I; I = J; J = t; }   // I real, J maybe dummy
           const bool realJ = J < nblk;
-          load(S0, I);
-          if (realJ) load(S1, J);
-          cp_wait();
+          if (bulk) {
+            // one thread streams both blocks in with the TMA engine; the
+            // others zero the slots of missing columns (rows < m)
+            const int nI = min(B, s - I * B), nJ = realJ ? min(B, s - J * B) : 0;
+            if (threadIdx.x == 0) {
+              mbar_expect_tx(&ld_bar, (unsigned)((nI + nJ) * m * 8));
+              for (int c = 0; c < nI; ++c) bulk_g2s(S0 + c * MP, P.X + (size_t)(I * B + c) * P.ldx, m * 8, &ld_bar);
+              for (int c = 0; c < nJ; ++c) bulk_g2s(S1 + c * MP, P.X + (size_t)(J * B + c) * P.ldx, m * 8, &ld_bar);
+            }
+            for (int c = nI + warp; c < B; c += nw)
+              for (int q = lane; q < m; q += 32) S0[c * MP + q] = 0.0;
+            if (realJ)
+              for (int c = nJ + warp; c < B; c += nw)
+                for (int q = lane; q < m; q += 32) S1[c * MP + q] = 0.0;
+            if (threadIdx.x < 32) { dirt[0][threadIdx.x & 15] = 0; dirt[1][threadIdx.x & 15] = 0; }
+            mbar_wait(&ld_bar, ld_phase);
+            ld_phase ^= 1u;
+          } else {
+            load(S0, I);
+            if (realJ) load(S1, J);
+            cp_wait();
+            if (threadIdx.x < 32) { dirt[0][threadIdx.x & 15] = 1; dirt[1][threadIdx.x & 15] = 1; }
+          }
           __syncthreads();
-          norms_of(S0, 0);
-          if (realJ) norms_of(S1, 1);
+          norms_of(S0, 0, I);
+          if (realJ) norms_of(S1, 1, J);
           else if (threadIdx.x < 16) nrm[1][threadIdx.x] = 0.0;   // dummy block: nothing rotates
           __syncthreads();
           tick(c_load);
@@ -441,19 +518,38 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
                 if (rotate_regs<RPL>(xa, xb, al, be, dp, ip, dq, iq, tol, tiny2, d2, any)) {
                   dirty = true;
                   st_col(xb, S1 + q * MP);
-                  if (lane == 0) { nrm[1][q] = be; scl[1][q] = dq; iscl[1][q] = iq; }
+                  if (lane == 0) { nrm[1][q] = be; scl[1][q] = dq; iscl[1][q] = iq; dirt[1][q] = 1; }
                 }
               }
             }
             if (dirty) {
               st_col(xa, S0 + p * MP);
-              if (lane == 0) { scl[0][p] = dp; iscl[0][p] = ip; }
+              if (lane == 0) { scl[0][p] = dp; iscl[0][p] = ip; dirt[0][p] = 1; }
             }
           }
           __syncthreads();
           tick(c_cross);
-          store(S0, 0, I);
-          if (realJ) store(S1, 1, J);
+          if (bulk) {
+            // rotated columns go back as they are (scaled form) with their
+            // scales; unrotated columns are unchanged in global memory
+            const int nI = min(B, s - I * B), nJ = realJ ? min(B, s - J * B) : 0;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) {
+              for (int c = 0; c < nI; ++c)
+                if (dirt[0][c]) bulk_s2g(P.X + (size_t)(I * B + c) * P.ldx, S0 + c * MP, m * 8);
+              for (int c = 0; c < nJ; ++c)
+                if (dirt[1][c]) bulk_s2g(P.X + (size_t)(J * B + c) * P.ldx, S1 + c * MP, m * 8);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (threadIdx.x < nI && dirt[0][threadIdx.x]) P.sigma[I * B + threadIdx.x] = scl[0][threadIdx.x];
+            if (threadIdx.x >= 32 && threadIdx.x < 32 + nJ && dirt[1][threadIdx.x - 32])
+              P.sigma[J * B + threadIdx.x - 32] = scl[1][threadIdx.x - 32];
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          } else {
+            store(S0, 0, I);
+            if (realJ) store(S1, 1, J);
+          }
           __syncthreads();
           tick(c_store);
         }
@@ -489,6 +585,9 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   // ---- singular values = column norms; sort descending; normalise
   double* sig = sm;                // s values (shared memory reused)
   int* perm = (int*)(sm + s);
+  double* dsc = sm + s + (s + 1) / 2;   // column scales (after perm)
+  for (int c = threadIdx.x; c < s; c += nthr) dsc[c] = __ldcg(P.sigma + c);
+  __syncthreads();
   for (int c = warp; c < s; c += nw) {
     double a = 0.0;
     for (int r = lane; r < m; r += 32) {
@@ -496,7 +595,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
       a = fma(x, x, a);
     }
     a = wsum(a);
-    if (lane == 0) sig[c] = sqrt(a);
+    if (lane == 0) sig[c] = sqrt(a) * dsc[c];
   }
   __syncthreads();
   for (int c = threadIdx.x; c < s; c += nthr) {
@@ -512,7 +611,7 @@ __global__ void __launch_bounds__(NT) jacobi_cluster_kernel(const JacobiProb* __
   for (int pos = warp; pos < s; pos += nw) {
     const int c = perm[pos];
     const double v = sig[c];
-    const double inv = v > 0.0 ? 1.0 / v : 0.0;
+    const double inv = v > 0.0 ? dsc[c] / v : 0.0;
     for (int r = lane; r < m; r += 32)
       P.Vout[(size_t)pos * P.ldv + r] = __ldcg(P.X + (size_t)c * P.ldx + r) * inv;
     if (lane == 0) P.sigma[pos] = v;
@@ -628,7 +727,7 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     const int K = mmax <= 768 ? 2 : 1;
     const int bmax = mmax <= 768 ? 14 : mmax <= 1024 ? 8 : 4;
     if (Bg > bmax) Bg = bmax;
-    const size_t smem = std::max((size_t)2 * Bg * MP * 8, (size_t)smax * 12 + 64);
+    const size_t smem = std::max((size_t)2 * Bg * MP * 8, (size_t)smax * 20 + 64);
     TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     double by = 0;
