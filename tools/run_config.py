@@ -32,14 +32,19 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--z-normal", action="store_true",
+                    help="z = default_rng(1).standard_normal(n) (timing only; C4/C5 cannot be "
+                         "sampled densely on one GPU)")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     out = {"config": a.config, **{k: v for k, v in c.items()}}
     locs = tb.generate_locations(c["n"], 0)
     p = tb.MaternParams(*c["theta"])
     t0 = time.perf_counter()
-    z = tb.sample_measurements(locs, p, 1)
+    z = (np.random.default_rng(1).standard_normal(c["n"]) if a.z_normal
+         else tb.sample_measurements(locs, p, 1))
     out["sample_s"] = time.perf_counter() - t0
+    out["z"] = "standard normal (timing only)" if a.z_normal else "sample_measurements(locs, theta, 1)"
     cfg = tb.LikelihoodConfig(mode="tlr", accuracy=c["acc"], nb=c["nb"], max_rank=c["max_rank"])
     ts = []
     for _ in range(a.repeats):
