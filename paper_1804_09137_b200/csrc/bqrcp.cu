@@ -258,8 +258,11 @@ __global__ void __launch_bounds__(512) bq_pick_reg_kernel(const QrcpProb* __rest
 #pragma unroll
   for (int r = 0; r < L; ++r) cn = fma(x[r], x[r], cn);
   bool sel = !own;
-  __shared__ double colb[L], v[L], red[16];
-  __shared__ int redi[16], chosen[32], arr[512], pos[512], piv[32];
+  // each warp publishes its best candidate column speculatively, so a step
+  // needs two barriers: (warp candidates) -> (warp 0: global argmax +
+  // reflector) -> (update)
+  __shared__ double slot[16 * L], v[L], wbest[16];
+  __shared__ int widx[16], chosen[32], arr[512], pos[512], piv[32];
   __shared__ double s_tau;
   for (int t = 0; t < bb; ++t) {
     double best = sel ? -1.0 : cn;
@@ -270,28 +273,25 @@ __global__ void __launch_bounds__(512) bq_pick_reg_kernel(const QrcpProb* __rest
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    if (lane == 0) { red[warp] = best; redi[warp] = bi; }
+    if (c == bi) {
+#pragma unroll
+      for (int r = 0; r < L; ++r) slot[warp * L + r] = x[r];
+    }
+    if (lane == 0) { wbest[warp] = best; widx[warp] = bi; }
     __syncthreads();
     if (warp == 0) {
-      best = lane < nw ? red[lane] : -1.0;
-      bi = lane < nw ? redi[lane] : 1 << 30;
+      double gb = lane < nw ? wbest[lane] : -1.0;
+      int gi = lane < nw ? widx[lane] : 1 << 30;
+      int gw = lane;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        const double ob = __shfl_xor_sync(0xffffffffu, gb, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        const int ow = __shfl_xor_sync(0xffffffffu, gw, o);
+        if (ob > gb || (ob == gb && oi < gi)) { gb = ob; gi = oi; gw = ow; }
       }
-      if (lane == 0) chosen[t] = bi;
-    }
-    __syncthreads();
-    const int pc = chosen[t];
-    if (c == pc) {
-      sel = true;
-#pragma unroll
-      for (int r = 0; r < L; ++r) colb[r] = x[r];
-    }
-    __syncthreads();
-    if (warp == 0) {
+      if (lane == 0) chosen[t] = gi;
+      const double* colb = slot + gw * L;
       double ss = 0.0;
       for (int r = t + 1 + lane; r < L; r += 32) ss = fma(colb[r], colb[r], ss);
       ss = wsum_b(ss);
@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(512) bq_pick_reg_kernel(const QrcpProb* __rest
       if (lane == 0) s_tau = tau;
     }
     __syncthreads();
+    if (c == chosen[t]) sel = true;
     if (!sel) {
       // volatile reads: the reflector is re-read from shared memory in both
       // passes instead of being held in registers (x[] already takes 2L)
@@ -370,16 +371,26 @@ __global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restric
   const int bb = min(b, min(nr, mr));
   double* Pn = sm;                       // mr x bb, ld mr
   __shared__ double tau_s[32], G[32 * 32], Ts[32 * 32], red[33];
-  __shared__ double s_beta, s_scale;
+  __shared__ double s_scale;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int c = 0; c < bb; ++c)
     for (int r = tid; r < mr; r += blockDim.x) Pn[c * mr + r] = P.A[(size_t)(j + c) * P.lda + j + r];
   __syncthreads();
-  for (int t = 0; t < bb; ++t) {
+  // One barrier per column: the reflector of column t is formed by warp 0
+  // from the norm of column t below row t, which the warp that updated column
+  // t in step t-1 computed (look-ahead); column t itself is scaled into v_t
+  // after the barrier that ends step t, when no warp reads it any more.
+  __shared__ double s_ss, beta_s[32];
+  {
     double a = 0.0;
-    for (int r = t + 1 + tid; r < mr; r += blockDim.x) a = fma(Pn[t * mr + r], Pn[t * mr + r], a);
-    const double ss = block_sum(a, red);
+    for (int r = 1 + tid; r < mr; r += blockDim.x) a = fma(Pn[r], Pn[r], a);
+    const double ss0 = block_sum(a, red);
+    if (tid == 0) s_ss = ss0;
+  }
+  __syncthreads();
+  for (int t = 0; t < bb; ++t) {
     if (tid == 0) {
+      const double ss = s_ss;
       const double alpha = Pn[t * mr + t];
       double tau = 0.0, scale = 0.0, beta = alpha;
       if (ss != 0.0) {
@@ -388,24 +399,37 @@ __global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restric
         scale = 1.0 / (alpha - beta);
       }
       tau_s[t] = tau;
-      s_beta = beta;
+      beta_s[t] = beta;
       s_scale = scale;
     }
     __syncthreads();
-    const double scale = s_scale;
-    for (int r = t + 1 + tid; r < mr; r += blockDim.x) Pn[t * mr + r] *= scale;
-    __syncthreads();
-    if (tid == 0) Pn[t * mr + t] = s_beta;
-    const double tau = tau_s[t];
+    const double scale = s_scale, tau = tau_s[t];
+    // columns c > t: w = tau (x_t + scale sum_{r>t} a_r x_r), x -= w v_t
     for (int c = t + 1 + warp; c < bb; c += nw) {
       double w = 0.0;
       for (int r = t + 1 + lane; r < mr; r += 32) w = fma(Pn[t * mr + r], Pn[c * mr + r], w);
-      w = (wsum_b(w) + Pn[c * mr + t]) * tau;
+      w = (wsum_b(w) * scale + Pn[c * mr + t]) * tau;
+      const double ws_ = w * scale;
+      double a = 0.0;
+      for (int r = t + 1 + lane; r < mr; r += 32) {
+        const double y = fma(-ws_, Pn[t * mr + r], Pn[c * mr + r]);
+        Pn[c * mr + r] = y;
+        if (c == t + 1 && r > t + 1) a = fma(y, y, a);
+      }
+      if (c == t + 1) {
+        a = wsum_b(a);
+        if (lane == 0) s_ss = a;   // read by thread 0 after the next barrier
+      }
       if (lane == 0) Pn[c * mr + t] -= w;
-      for (int r = t + 1 + lane; r < mr; r += 32) Pn[c * mr + r] -= w * Pn[t * mr + r];
     }
     __syncthreads();
+    // column t -> reflector storage (nobody reads it during step t + 1)
+    if (warp == nw - 1) {
+      for (int r = t + 1 + lane; r < mr; r += 32) Pn[t * mr + r] *= scale;
+      if (lane == 0) Pn[t * mr + t] = beta_s[t];
+    }
   }
+  __syncthreads();
   // write back R / reflectors, explicit V
   double* V = ws + (size_t)blockIdx.x * wsz + off_v;
   for (int c = 0; c < bb; ++c)

@@ -41,7 +41,7 @@ struct Profiler {
   unsigned mask = ~0u;   // kernel classes timed while on (tlrb_profile_mask)
   double ms[K_NCLASS] = {}, flops[K_NCLASS] = {}, bytes[K_NCLASS] = {};
   int64_t count[K_NCLASS] = {};
-  struct Pend { int cls; cudaEvent_t a, b; cudaStream_t s; };
+  struct Pend { int cls; cudaEvent_t a, b; cudaStream_t s; double fl; };
   cudaEvent_t epoch = nullptr;   // TLRB_TIMELINE=path: per-launch (class, start, end) dump
   std::vector<Pend> pend;
   std::vector<cudaEvent_t> pool;

@@ -33,7 +33,7 @@ void Profiler::end(cudaStream_t s, double fl, double by) {
   if (open_cls < 0) return;
   cudaEvent_t b = get();
   TLRB_CUDA(cudaEventRecord(b, s));
-  pend.push_back({open_cls, open_ev, b, s});
+  pend.push_back({open_cls, open_ev, b, s, fl});
   flops[open_cls] += fl;
   bytes[open_cls] += by;
   count[open_cls] += 1;
@@ -47,7 +47,7 @@ void Profiler::drain() {
     if (cudaEventElapsedTime(&a, p.a, p.b) == cudaSuccess) ms[p.cls] += a;
     float t0 = 0;
     if (tl && cudaEventElapsedTime(&t0, epoch, p.a) == cudaSuccess)
-      fprintf(tl, "%s %.4f %.4f %p\n", kclass_name[p.cls], t0, t0 + a, (void*)p.s);
+      fprintf(tl, "%s %.4f %.4f %p %.6g\n", kclass_name[p.cls], t0, t0 + a, (void*)p.s, p.fl);
     pool.push_back(p.a);
     pool.push_back(p.b);
   }

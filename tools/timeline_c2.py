@@ -27,7 +27,7 @@ _lib.profile_enable(True)
 h.loglik(z, p, acc)
 _lib.profile_read()
 rows = [ln.split() for ln in open(path)]
-ev = sorted((float(a), float(b), c) for c, a, b, _ in rows)
+ev = sorted((float(a), float(b), c) for c, a, b, *_ in rows)
 t0 = ev[0][0]
 end = max(b for _, b, _ in ev)
 
@@ -64,3 +64,26 @@ for k in range(nb):
         fr.append(union(iv) / B)
     anyiv = [(max(a, lo), min(b, hi)) for a, b, _ in ev if b > lo and a < hi]
     print(f"{k * B:8.0f}   " + " ".join(f"{f:6.2f}" for f in fr) + f"  {1 - union(anyiv) / B:5.2f}")
+# GEMM launches: achieved TFLOP/s distribution (weighted by time)
+g = [(float(b) - float(a), float(r[4])) for r in rows for (c, a, b) in [(r[0], r[1], r[2])] if c == "dgemm_vbatch" and len(r) > 4]
+if g:
+    import collections
+    bins = collections.defaultdict(lambda: [0.0, 0.0, 0])
+    for dt, fl in g:
+        tf = fl / (dt * 1e-3) / 1e12 if dt > 0 else 0.0
+        k = "<0.5" if tf < 0.5 else "<2" if tf < 2 else "<5" if tf < 5 else "<10" if tf < 10 else "<20" if tf < 20 else ">=20"
+        bins[k][0] += dt; bins[k][1] += fl; bins[k][2] += 1
+    print("GEMM launches by achieved TFLOP/s: bucket  ms  GFLOP  launches")
+    for k in ("<0.5", "<2", "<5", "<10", "<20", ">=20"):
+        if k in bins:
+            v = bins[k]
+            print(f"  {k:5s} {v[0]:8.2f} {v[1] / 1e9:9.2f} {v[2]:6d}")
+# optional window listing: TL_WINDOW="t0,t1" (ms relative to the first launch)
+win = os.environ.get("TL_WINDOW")
+if win:
+    lo, hi = (float(v) for v in win.split(","))
+    print(f"launches in [{lo}, {hi}] ms:")
+    for r in sorted(rows, key=lambda r: float(r[1])):
+        a, b = float(r[1]) - t0, float(r[2]) - t0
+        if b >= lo and a <= hi:
+            print(f"  {a:9.3f} {b:9.3f} {1e3 * (b - a):8.1f} us  {r[0]:15s} {r[3][-6:]}  {float(r[4]) / 1e9 if len(r) > 4 else 0:8.3f} GF")
