@@ -26,6 +26,7 @@
 #include <cfloat>
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <algorithm>
 
 namespace cg = cooperative_groups;
 
@@ -678,6 +679,11 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
       for (const JacobiProb& p : groups[g]) groups[g - 1].push_back(p);
       groups[g].clear();
     }
+  // longest first inside a group (cost ~ s^2): clusters are dispatched in
+  // grid order, so the big matrices start in the first wave and the short
+  // ones fill the tail
+  for (auto& g : groups)
+    std::stable_sort(g.begin(), g.end(), [](const JacobiProb& x, const JacobiProb& y) { return x.s > y.s; });
   // independent problem groups run concurrently: the largest-cluster group
   // on the caller's stream, the others on side streams forked/joined with
   // events (they would otherwise serialise behind each other)
