@@ -662,11 +662,15 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     const int v = e ? atoi(e) : 16;
     return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0;
   }();
+  // 16-CTA clusters only for the largest matrices: at most 7 of them are
+  // co-resident (112 SMs), so mid-size matrices (up to cl16_pairs block
+  // pairs) take 8-CTA clusters and run beside them on the remaining SMs
+  static const int cl16_pairs = getenv("TLRB_JACOBI_CL16_PAIRS") ? atoi(getenv("TLRB_JACOBI_CL16_PAIRS")) : 8;
   std::vector<JacobiProb> groups[5];
   for (const JacobiProb& p : probs) {
     const int nblk = (p.s + B - 1) / B;
     const int pairs = (nblk + 1) / 2;
-    int g = pairs <= 1 ? 0 : pairs <= 2 ? 1 : pairs <= 4 ? 2 : pairs <= 8 ? 3 : 4;
+    int g = pairs <= 1 ? 0 : pairs <= 2 ? 1 : pairs <= 4 ? 2 : pairs <= cl16_pairs ? 3 : 4;
     g = std::min(g, max_g);
     groups[g].push_back(p);
   }
