@@ -279,6 +279,24 @@ def main():
         e2e.append(allmax(time.perf_counter() - t0))
     e2e_s = float(np.median(e2e))
 
+    # variants (other accuracies / dense): every rank takes part, since a
+    # distributed handle runs NCCL collectives inside each evaluation
+    var = None
+    if not args.no_variants:
+        var = {}
+        for acc in ([0.0, 1e-7, 1e-5] if args.acc else [1e-9, 1e-7, 1e-5]):
+            if acc == args.acc:
+                continue
+            one(acc)
+            tt = []
+            for _ in range(2):
+                ll_v, _, _ = one(acc)
+                tt.append(allmax(h.last_stats["ms_device"]))
+            r = REF_LL.get(ref_key(acc))
+            var[mode_key(acc)] = {"s": float(np.median(tt)) * 1e-3, "ll": ll_v, "ref_ll": r,
+                                  "rel": abs(ll_v - r) / abs(r) if r else None,
+                                  "max_rank": h.last_stats["max_rank"]}
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -341,20 +359,7 @@ def main():
     clk_s = clk.summary()
     if clk_s:
         line["clocks"] = clk_s
-    if not args.no_variants:
-        var = {}
-        for acc in ([0.0, 1e-7, 1e-5] if args.acc else [1e-9, 1e-7, 1e-5]):
-            if acc == args.acc:
-                continue
-            one(acc)
-            tt = []
-            for _ in range(2):
-                ll_v, _, _ = one(acc)
-                tt.append(h.last_stats["ms_device"])
-            r = REF_LL.get(ref_key(acc))
-            var[mode_key(acc)] = {"s": float(np.median(tt)) * 1e-3, "ll": ll_v, "ref_ll": r,
-                                  "rel": abs(ll_v - r) / abs(r) if r else None,
-                                  "max_rank": h.last_stats["max_rank"]}
+    if var is not None:
         line["variants"] = var
     if not args.no_cpu:
         # in a fresh interpreter (no torch / CUDA runtime threads next to the
