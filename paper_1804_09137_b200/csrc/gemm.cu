@@ -11,6 +11,7 @@
 // tiles; BK = 16; operands staged global -> registers -> shared memory with a
 // two-stage ping-pong so the next K slab loads while DMMAs run.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace tlrb {
 
@@ -162,11 +163,17 @@ void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, 
 
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
+  // large plain problems go to the CUTLASS grouped DMMA kernel (gemm_cutlass.cu);
+  // lower-only, flagged and skinny ones stay here (TLRB_GEMM_CUTLASS=0: all here)
+  static const bool use_cutlass = have_cutlass_gemm() && !(getenv("TLRB_GEMM_CUTLASS") &&
+                                                           atoi(getenv("TLRB_GEMM_CUTLASS")) == 0);
+  const std::vector<GemmProb> rest = use_cutlass ? launch_gemm_cutlass(probs, ar, s) : probs;
+  if (rest.empty()) return;
   std::vector<GemmProb> keep;
   std::vector<int> start;
-  keep.reserve(probs.size());
-  start.reserve(probs.size() + 1);
-  const GemmStaged g = stage_gemm(probs, keep, start);
+  keep.reserve(rest.size());
+  start.reserve(rest.size() + 1);
+  const GemmStaged g = stage_gemm(rest, keep, start);
   if (g.tot == 0) return;
   const GemmProb* dp = ar.put(keep, s);
   const int* ds = ar.put(start, s);
