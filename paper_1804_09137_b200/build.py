@@ -42,10 +42,33 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+OBJ = PKG.parent / "build" / "obj"
+
+
+def _compile(src: Path, force: bool, verbose: bool) -> Path:
+    """One translation unit -> build/obj/<name>.o (rebuilt when the source or
+    any shared header is newer)."""
+    obj = OBJ / (src.stem + ".o")
+    hdrs = sorted((PKG / "csrc").glob("*.cuh")) + [PKG.parent / "include" / "tlrb200.h"]
+    if not force and obj.exists() and all(p.stat().st_mtime <= obj.stat().st_mtime for p in [src, *hdrs]):
+        return obj
+    flags = [f for f in FLAGS if f != "-shared"]
+    cmd = [NVCC, *flags, "-c", str(src), "-o", str(obj)]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return obj
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC, *FLAGS, *map(str, SRC), "-o", str(OUT), "-lnccl"]
+    from concurrent.futures import ThreadPoolExecutor
+    OBJ.mkdir(parents=True, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=min(len(SRC), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force, verbose), SRC))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           *map(str, objs), "-o", str(OUT), "-lnccl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -316,6 +316,9 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     for (int j = 0; j < nj; ++j) { rmax = std::max(rmax, rr[j]); smax = std::max(smax, sw[j]); }
     fprintf(stderr, "[tlrb] compress nj=%d  qrcp %.2f ms  jacobi %.2f ms  rmax=%d sweeps<=%d\n", nj,
             t_q1 - t_q0, now_ms() - t_q1, rmax, smax);
+    if (getenv("TLRB_TRACE_JOBS"))   // per job: m n qrcp-rank final-rank sweeps
+      for (int j = 0; j < nj; ++j)
+        fprintf(stderr, "[job] %d %d %d %d %d\n", jobs[j].m, jobs[j].n, rr[j], rk[j], sw[j]);
   }
   std::vector<GemmProb> gu;
   std::vector<CopyProb> cv;
