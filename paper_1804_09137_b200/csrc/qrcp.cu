@@ -536,8 +536,13 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   for (const QrcpProb& p : probs) { mmax = std::max(mmax, p.m); nmax = std::max(nmax, p.n); }
   int CL = 0;
   const bool cluster_ok = !no_cluster && cluster_cpc(mmax, nmax, CL) > 0;
+  // blocked path available for every tile size up to 2048 (the panel of b
+  // columns fits in shared memory); the cluster kernel only while a matrix
+  // fits in the shared memory of a 16-CTA cluster (nb <= ~500)
+  static const int blocked_min = getenv("TLRB_QRCP_BLOCKED") ? atoi(getenv("TLRB_QRCP_BLOCKED")) : 8;
+  const bool blocked_ok = blocked_min > 0 && mmax <= 2048 && nmax <= 2048;
   for (size_t i = 0; i < probs.size(); ++i) {
-    if (cluster_ok && probs[i].hint > thr) { big.push_back(probs[i]); big_idx.push_back((int)i); }
+    if ((cluster_ok || blocked_ok) && probs[i].hint > thr) { big.push_back(probs[i]); big_idx.push_back((int)i); }
     else small.push_back(probs[i]);
   }
   // large problems: blocked randomized QRCP (bqrcp.cu), GEMM-based and not
@@ -545,8 +550,10 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   // The cluster kernel has the lower latency for a lone matrix, the blocked
   // one the higher throughput: it is used once the big problems exceed the
   // clusters that can be co-resident (7 of 16 CTAs on 148 SMs).
-  static const int blocked_min = getenv("TLRB_QRCP_BLOCKED") ? atoi(getenv("TLRB_QRCP_BLOCKED")) : 8;
-  if (blocked_min > 0 && (int)big.size() >= blocked_min && mmax <= 2048 && nmax <= 2048) {
+  // Without the cluster kernel (large tiles) the blocked path takes the big
+  // problems at any batch size: a one-CTA QRCP of a 760 x 760 matrix streams
+  // the whole trailing matrix through one SM at every pivot.
+  if (blocked_ok && !big.empty() && ((int)big.size() >= blocked_min || !cluster_ok)) {
     const QrcpLaunch Ls = stage(small, ar, s);
     if (!Ls.count) { launch_qrcp_blocked(big, ar, s); return; }
     static cudaStream_t side2 = nullptr;
