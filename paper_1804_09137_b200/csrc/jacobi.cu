@@ -650,12 +650,14 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     return true;
   }();
   (void)early_set;
+  // staged column stride MP = 32 RPL of the instantiation (per group below)
+  auto stride_of = [](int m) {
+    return m <= 128 ? 128 : m <= 256 ? 256 : m <= 384 ? 384 : m <= 512 ? 512 : m <= 768 ? 768 : m <= 1024 ? 1024 : 2048;
+  };
   int mmax = 1;
   for (const JacobiProb& p : probs) mmax = std::max(mmax, p.m);
-  // staged column stride MP = 32 RPL of the instantiation chosen below
-  const int MP = mmax <= 512 ? 512 : mmax <= 768 ? 768 : mmax <= 1024 ? 1024 : 2048;
   int B = 16;
-  while (B > 2 && (size_t)2 * B * MP * 8 > 227 * 1024 - 1024) --B;
+  while (B > 2 && (size_t)2 * B * stride_of(mmax) * 8 > 227 * 1024 - 1024) --B;
   // group by cluster size: one CTA per block pair of a round, at most 8
   static int max_g = [] {
     const char* e = getenv("TLRB_JACOBI_MAXCL");
@@ -722,8 +724,9 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
       }
     }
     const int CL = 1 << g;
-    int smax = 1;
-    for (const JacobiProb& p : groups[g]) smax = std::max(smax, p.s);
+    int smax = 1, gm = 1;
+    for (const JacobiProb& p : groups[g]) { smax = std::max(smax, p.s); gm = std::max(gm, p.m); }
+    const int MP = stride_of(gm);
     // block width so that a round has (close to) one block pair per CTA:
     // nblk = 2 CL blocks of width ceil(smax / 2CL), even, <= B
     int Bg = (smax + 2 * CL - 1) / (2 * CL);
@@ -731,11 +734,14 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     // rows per lane and the thread bound (registers: 2 RPL doubles per lane)
     // K = 2 (two register columns per warp, B/2 warps) where the registers
     // allow it; one column per warp for the long columns
-    auto kern = mmax <= 512 ? jacobi_cluster_kernel<16, 256, 2>
-              : mmax <= 768 ? jacobi_cluster_kernel<24, 256, 2>
-              : mmax <= 1024 ? jacobi_cluster_kernel<32, 256, 1> : jacobi_cluster_kernel<64, 128, 1>;
-    const int K = mmax <= 768 ? 2 : 1;
-    const int bmax = mmax <= 768 ? 14 : mmax <= 1024 ? 8 : 4;
+    auto kern = gm <= 128 ? jacobi_cluster_kernel<4, 256, 2>
+              : gm <= 256 ? jacobi_cluster_kernel<8, 256, 2>
+              : gm <= 384 ? jacobi_cluster_kernel<12, 256, 2>
+              : gm <= 512 ? jacobi_cluster_kernel<16, 256, 2>
+              : gm <= 768 ? jacobi_cluster_kernel<24, 256, 2>
+              : gm <= 1024 ? jacobi_cluster_kernel<32, 256, 1> : jacobi_cluster_kernel<64, 128, 1>;
+    const int K = gm <= 768 ? 2 : 1;
+    const int bmax = gm <= 768 ? 14 : gm <= 1024 ? 8 : 4;
     if (Bg > bmax) Bg = bmax;
     const size_t smem = std::max((size_t)2 * Bg * MP * 8, (size_t)smax * 20 + 64);
     TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -78,8 +78,9 @@ void DescArena::release() {
 void* DescArena::put_bytes(const void* src, size_t bytes, cudaStream_t s) {
   const size_t a = (off_ + 255) & ~(size_t)255;
   if (a + bytes > cap_) {
-    // arena full: wait for the stream so earlier descriptors are consumed
-    TLRB_CUDA(cudaStreamSynchronize(s));
+    // arena full: wait until earlier descriptors are consumed (every stream
+    // of the device may hold some: look-ahead / side streams)
+    TLRB_CUDA(cudaDeviceSynchronize());
     off_ = 0;
     return put_bytes(src, bytes, s);
   }

@@ -54,6 +54,10 @@ struct Flops {
 struct tlrb_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // look-ahead stream: POTRF of the next diagonal tile overlaps the current
+  // step's recompressions (factor_tlr)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_syrk = nullptr, ev_potrf = nullptr;
   cudaEvent_t ev[6];
   int64_t n = 0;
   int nb = 0, t = 0, cap = 0, max_rank = 0;
@@ -145,6 +149,9 @@ struct tlrb_handle {
   double* D(int i) const { return diag + (size_t)i * nb * nb; }
   void sync() {
     TLRB_CUDA(cudaStreamSynchronize(stream));
+    // the arena is reset below: descriptors queued on the look-ahead stream
+    // must have been consumed too
+    if (side) TLRB_CUDA(cudaStreamSynchronize(side));
     ar.reset();
     if (g_prof.on) g_prof.drain();
   }
@@ -412,7 +419,8 @@ void compress_all(tlrb_handle* h, double acc) {
 }
 
 // ------------------------------------------------------------------ POTRF
-void potrf(tlrb_handle* h, int k) {
+void potrf(tlrb_handle* h, int k, cudaStream_t s = nullptr) {
+  if (!s) s = h->stream;
   if (!h->own(k, k)) {   // L_kk arrives from its owner
     bcast(h, h->D(k), (size_t)h->nb * h->nb, h->owner(k, k));
     return;
@@ -421,14 +429,14 @@ void potrf(tlrb_handle* h, int k) {
   double* A = h->D(k);
   for (int r0 = 0; r0 < n; r0 += kPotrfBlock) {
     const int bs = std::min(kPotrfBlock, n - r0);
-    launch_potrf_block(A, h->nb, n, r0, bs, k, h->d_info, h->d_logdiag + h->off[k], h->stream);
+    launch_potrf_block(A, h->nb, n, r0, bs, k, h->d_info, h->d_logdiag + h->off[k], s);
     const int rest = n - r0 - bs;
     if (rest > 0) {
       double* A21 = A + (size_t)r0 * h->nb + r0 + bs;
       double* A22 = A + (size_t)(r0 + bs) * h->nb + r0 + bs;
       launch_gemm({GemmProb{A21, A21, A22, A22, rest, rest, bs, h->nb, h->nb, h->nb, h->nb, 0, 1, 1,
                             -1.0, 1.0}},
-                  h->ar, h->stream);
+                  h->ar, s);
     }
   }
   const double nn = n;
@@ -465,6 +473,9 @@ bool check_npd(tlrb_handle* h) {
   }
   TLRB_CUDA(cudaMemcpyAsync(info, src, sizeof info, cudaMemcpyDeviceToHost, h->stream));
   h->sync();
+  if (info[0] && !h->dist()) {   // a look-ahead POTRF may have been writing it: re-read settled
+    TLRB_CUDA(cudaMemcpy(info, src, sizeof info, cudaMemcpyDeviceToHost));
+  }
   if (info[0]) {
     h->err_tile = info[1];
     h->err_pivot = info[2];
@@ -515,9 +526,14 @@ bool factor_dense(tlrb_handle* h) {
 bool factor_tlr(tlrb_handle* h, double acc) {
   const int t = h->t, nb = h->nb;
   double* tmp = reinterpret_cast<double*>(h->ws);  // small products before the job batch
+  // POTRF(k+1) only needs step k's SYRK of D(k+1): it runs on the look-ahead
+  // stream while step k's recompressions run (single-GPU handles)
+  static const bool lookahead = !(getenv("TLRB_LOOKAHEAD") && atoi(getenv("TLRB_LOOKAHEAD")) == 0);
+  int ahead = -1;
   for (int k = 0; k < t; ++k) {
     const double tk0 = trace_on() ? now_ms() : 0;
-    potrf(h, k);
+    if (ahead == k) TLRB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_potrf, 0));
+    else potrf(h, k);
     // K4: V_ik <- L_kk^-1 V_ik (low-rank) / L_ik^T <- L_kk^-1 A_ik^T (dense, A13)
     std::vector<TrsmProb> tp;
     for (int i = k + 1; i < t; ++i) {
@@ -571,6 +587,13 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_gemm(g1, h->ar, h->stream);
       launch_gemm(g2, h->ar, h->stream);
       launch_gemm(g3, h->ar, h->stream);
+    }
+    if (lookahead && !h->dist() && k + 1 < t) {
+      TLRB_CUDA(cudaEventRecord(h->ev_syrk, h->stream));
+      TLRB_CUDA(cudaStreamWaitEvent(h->side, h->ev_syrk, 0));
+      potrf(h, k + 1, h->side);
+      TLRB_CUDA(cudaEventRecord(h->ev_potrf, h->side));
+      ahead = k + 1;
     }
     if (trace_on()) {
       h->sync();
@@ -1121,6 +1144,9 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     h->device = device;
     TLRB_CUDA(cudaSetDevice(device));
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    TLRB_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_syrk, cudaEventDisableTiming));
+    TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_potrf, cudaEventDisableTiming));
     for (auto& e : h->ev) TLRB_CUDA(cudaEventCreate(&e));
     h->n = n;
     h->nb = (int)std::min<int64_t>(nb, n);
@@ -1242,6 +1268,9 @@ void tlrb_destroy(tlrb_handle* h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_syrk) cudaEventDestroy(h->ev_syrk);
+  if (h->ev_potrf) cudaEventDestroy(h->ev_potrf);
   delete h;
 }
 
