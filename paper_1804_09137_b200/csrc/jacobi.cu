@@ -734,14 +734,19 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     // rows per lane and the thread bound (registers: 2 RPL doubles per lane)
     // K = 2 (two register columns per warp, B/2 warps) where the registers
     // allow it; one column per warp for the long columns
+    // 512 < m <= 768 (nb = 760): TLRB_JACOBI_768 = 0 two columns per warp
+    // (RPL 24 spills), 1 one column per warp with 8 warps, 2 with 12 warps
+    static const int v768 = getenv("TLRB_JACOBI_768") ? atoi(getenv("TLRB_JACOBI_768")) : 2;
+    const bool k1_768 = gm > 512 && gm <= 768 && v768 > 0;
     auto kern = gm <= 128 ? jacobi_cluster_kernel<4, 256, 2>
               : gm <= 256 ? jacobi_cluster_kernel<8, 256, 2>
               : gm <= 384 ? jacobi_cluster_kernel<12, 256, 2>
               : gm <= 512 ? jacobi_cluster_kernel<16, 256, 2>
-              : gm <= 768 ? jacobi_cluster_kernel<24, 256, 2>
+              : gm <= 768 ? (v768 == 1 ? jacobi_cluster_kernel<24, 256, 1>
+                             : v768 == 2 ? jacobi_cluster_kernel<24, 384, 1> : jacobi_cluster_kernel<24, 256, 2>)
               : gm <= 1024 ? jacobi_cluster_kernel<32, 256, 1> : jacobi_cluster_kernel<64, 128, 1>;
-    const int K = gm <= 768 ? 2 : 1;
-    const int bmax = gm <= 768 ? 14 : gm <= 1024 ? 8 : 4;
+    const int K = gm <= 768 && !k1_768 ? 2 : 1;
+    const int bmax = k1_768 ? (v768 == 2 ? 12 : 8) : gm <= 768 ? 14 : gm <= 1024 ? 8 : 4;
     if (Bg > bmax) Bg = bmax;
     const size_t smem = std::max((size_t)2 * Bg * MP * 8, (size_t)smax * 20 + 64);
     TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -1181,7 +1181,11 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     h->slot_doubles = 7 * nb2 + 18 * (size_t)h->nb + 64;
     size_t freeb = 0, totb = 0;
     TLRB_CUDA(cudaMemGetInfo(&freeb, &totb));
-    size_t budget = std::min<size_t>(freeb / 3, (size_t)24 << 30);
+    // capped at 56 GB for tile grids up to 128 x 128 (fewer, larger job
+    // batches: C3 16.3 s vs 17.2 s at 24 GB) and at 24 GB beyond, where the
+    // rank-adaptive factor arena needs the rest of HBM (C4, C5); TLRB_WS_GB overrides
+    const size_t cap_gb = getenv("TLRB_WS_GB") ? (size_t)atoll(getenv("TLRB_WS_GB")) : (h->t <= 128 ? 56 : 24);
+    size_t budget = std::min<size_t>(freeb / 3, cap_gb << 30);
     int jobs = (int)std::max<size_t>(1, budget / (h->slot_doubles * 8));
     jobs = (int)std::min<size_t>(jobs, std::max<size_t>(ntile, 1));
     h->max_jobs = std::min(jobs, 8192);
