@@ -372,3 +372,24 @@ def test_loglik_blocked_qrcp_everywhere(tb, gold):
     ll = json.loads(res.stdout.strip().splitlines()[-1])
     ref = gold["loglik"]["C1"]["modes"]["tlr:1e-09"]["ll"]
     assert abs(ll - ref) <= 1e-8 * abs(ref), (ll, ref)
+
+
+def test_lookahead_potrf_identical(tb):
+    """The look-ahead POTRF (next diagonal tile on a side stream during the
+    current step's recompressions) changes the schedule, not the arithmetic:
+    the log-likelihood is bitwise the one of the in-order schedule."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_1804_09137_b200 as tb;"
+            "l = tb.generate_locations(2000, 3); z = np.random.default_rng(4).standard_normal(2000);"
+            "print(repr(tb.log_likelihood(l, z, tb.MaternParams(1.0, 0.1, 0.5),"
+            " tb.LikelihoodConfig(mode='tlr', accuracy=1e-9, nb=250))))")
+    out = []
+    for la in ("1", "0"):
+        env = dict(os.environ, TLRB_LOOKAHEAD=la, PYTHONPATH=str(GOLD.parents[1]))
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(r.stdout.strip().splitlines()[-1])
+    assert out[0] == out[1], out
