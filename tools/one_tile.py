@@ -7,13 +7,14 @@ import numpy as np
 import paper_1804_09137_b200 as tb
 from paper_1804_09137_b200 import _lib
 
+ACC = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-9
 locs = tb.generate_locations(10000, 0)
 xy = locs.coords
 a = tb.matern_block(xy[500:1000], xy[0:500], tb.MaternParams(1.0, 0.1, 0.5))
-u, v = tb.compress_tile(a, 1e-9)
+u, v = tb.compress_tile(a, ACC)
 _lib.profile_enable(True)
 t0 = time.perf_counter()
-u, v = tb.compress_tile(a, 1e-9)
+u, v = tb.compress_tile(a, ACC)
 dt = time.perf_counter() - t0
 prof = _lib.profile_read()
 print("rank", u.shape[1], "err", np.linalg.norm(a - u @ v.T) / np.linalg.norm(a), f"wall {dt*1e3:.1f} ms")
