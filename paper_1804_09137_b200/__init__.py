@@ -21,6 +21,8 @@ from .api import (  # noqa: F401
     predict,
     sample_measurements,
 )
+from .mle import EstimationError, EstimationResult, mle_fit  # noqa: F401
+from .experiments import holdout_experiment, mc_experiment, mc_summaries, mse  # noqa: F401
 from .dataio import (  # noqa: F401
     DataError,
     Dataset,
@@ -35,4 +37,6 @@ __all__ = [
     "generate_locations", "launch_count", "log_likelihood", "log_likelihood_parts",
     "matern_block", "predict", "sample_measurements",
     "DataError", "Dataset", "load_dataset", "partition_regions", "save_dataset",
+    "EstimationError", "EstimationResult", "mle_fit",
+    "holdout_experiment", "mc_experiment", "mc_summaries", "mse",
 ]

@@ -333,6 +333,12 @@ def distributed_handle(coords, nb: int, max_rank: int = 0, P: int | None = None,
 _HANDLES: dict = {}
 
 
+def _local_device() -> int:
+    """One process per GPU (torchrun): single-GPU handles go to LOCAL_RANK's device."""
+    import os
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus, radius: float = 0.0) -> Handle:
     key = (coords.__array_interface__["data"][0], coords.shape[0], int(nb), int(max_rank or 0), ngpus,
            radius)
@@ -343,7 +349,7 @@ def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus, radius: float = 0.
         if ngpus and ngpus > 1:   # one process per GPU under torch.distributed
             h = (coords, distributed_handle(coords, nb, max_rank or 0, radius=radius))
         else:
-            h = (coords, Handle(coords, nb, max_rank or 0, radius=radius))
+            h = (coords, Handle(coords, nb, max_rank or 0, device=_local_device(), radius=radius))
         _HANDLES[key] = h
     return h[1]
 
@@ -392,7 +398,7 @@ def sample_measurements(locs, p_true: MaternParams, seed: int) -> np.ndarray:
     standard normals (the reference's own stream, drawn on the host)."""
     coords = _coords_of(locs)
     n = coords.shape[0]
-    h = Handle(coords, min(DEFAULT_NB_DENSE, n), radius=_radius_of(locs))
+    h = Handle(coords, min(DEFAULT_NB_DENSE, n), device=_local_device(), radius=_radius_of(locs))
     try:
         h.factorize(p_true, None)
         w = np.random.default_rng(seed).standard_normal(n)

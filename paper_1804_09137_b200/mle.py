@@ -39,6 +39,17 @@ class EstimationResult:
     trace: list = field(repr=False, default_factory=list)
 
 
+class EstimationError(Exception):
+    """Every objective evaluation failed (stats.py:31-38): same message and
+    `last_theta` attribute as the reference."""
+
+    def __init__(self, last_theta):
+        self.last_theta = tuple(last_theta)
+        super().__init__(
+            f"no likelihood evaluation succeeded; last theta tried {self.last_theta}"
+        )
+
+
 class _Budget(Exception):
     pass
 
@@ -129,7 +140,8 @@ def mle_fit(locs, z, cfg: LikelihoodConfig, objective=None, max_evaluations: int
     except _Budget:
         pass
     if best["x"] is None or not math.isfinite(best["f"]):
-        raise RuntimeError(f"no likelihood evaluation succeeded ({len(trace)} tried)")
+        last = trace[-1].theta if trace else tuple(float(v) for v in x0)
+        raise EstimationError(last)
     x = best["x"]
     return EstimationResult(MaternParams(x[0], x[1], x[2], cfg.nugget), -best["f"], it, converged,
                             len(trace), trace)
