@@ -355,6 +355,15 @@ def main():
                  "jacobi_max_sweeps": st["jacobi_max_sweeps"], "stored_reals": st["stored_reals"]},
         "kernels": kernels,
         "fp64_peak_tflops_measured": p64,
+        # whole-evaluation roofline from the algorithmic work
+        # counted per op at execution ranks (min flops / bytes; the op sum of
+        # max(F/P64, B/BW) is bounded below by this max of the totals)
+        "step_roofline": {
+            "t_roof_s": max(st["flops"] / (p64 * 1e12), st["bytes"] / (peaks["hbm_gbs"] * 1e9)),
+            "frac": max(st["flops"] / (p64 * 1e12), st["bytes"] / (peaks["hbm_gbs"] * 1e9)) / value_s,
+            "gflop": st["flops"] / 1e9, "gb": st["bytes"] / 1e9,
+            "note": "algorithmic FP64 flops / HBM bytes of the whole evaluation (gen, compression, "
+                    "TLR Cholesky, solve; rank 0's counted work) against the measured DGEMM peak and MEASURED_PEAKS hbm_gbs"},
     }
     clk_s = clk.summary()
     if clk_s:
