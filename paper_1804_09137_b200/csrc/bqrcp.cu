@@ -529,11 +529,17 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
   const size_t off_v = (size_t)l * nmax, off_t = off_v + (size_t)mmax * b, off_w = off_t + (size_t)b * b,
                off_w2 = off_w + (size_t)b * nmax;
   const size_t wsz = (off_w2 + (size_t)b * nmax + 31) & ~(size_t)31;
-  static double* ws = nullptr;
-  static size_t ws_cap = 0;
-  static BqState* st = nullptr;
-  static int st_cap = 0;
-  static double* omega = nullptr;
+  static double* ws_d[kMaxDevices] = {};
+  static size_t ws_cap_d[kMaxDevices] = {};
+  static BqState* st_d[kMaxDevices] = {};
+  static int st_cap_d[kMaxDevices] = {};
+  static double* omega_d[kMaxDevices] = {};
+  const int dev = current_device();
+  double*& ws = ws_d[dev];
+  size_t& ws_cap = ws_cap_d[dev];
+  BqState*& st = st_d[dev];
+  int& st_cap = st_cap_d[dev];
+  double*& omega = omega_d[dev];
   constexpr int kOmegaCols = 2048;
   if ((size_t)np * wsz > ws_cap) {
     if (ws) TLRB_CUDA(cudaFree(ws));

@@ -150,6 +150,17 @@ struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid
 
 // Device-resident descriptor staging (pinned host ring -> device), reset at
 // stream synchronisation points.
+// Launcher-side caches (side streams, events, scratch) are kept per device:
+// a process may drive handles on several GPUs (calls on one device are
+// serialised by the C ABI, tlrb.cu).
+constexpr int kMaxDevices = 16;
+inline int current_device() {
+  int d = 0;
+  TLRB_CUDA(cudaGetDevice(&d));
+  if (d < 0 || d >= kMaxDevices) throw CudaError(cudaErrorInvalidDevice, "device index >= 16", __FILE__, __LINE__);
+  return d;
+}
+
 class DescArena {
  public:
   void init(size_t bytes);

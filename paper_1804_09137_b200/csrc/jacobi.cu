@@ -693,8 +693,12 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
   // independent problem groups run concurrently: the largest-cluster group
   // on the caller's stream, the others on side streams forked/joined with
   // events (they would otherwise serialise behind each other)
-  static cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
-  static cudaEvent_t fork_ev = nullptr, join_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  static cudaStream_t side_d[kMaxDevices][4] = {};
+  static cudaEvent_t fork_d[kMaxDevices] = {}, join_d[kMaxDevices][4] = {};
+  const int dev = current_device();
+  cudaStream_t* side = side_d[dev];
+  cudaEvent_t& fork_ev = fork_d[dev];
+  cudaEvent_t* join_ev = join_d[dev];
   if (!fork_ev) {
     TLRB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
     for (int i = 0; i < 4; ++i) {

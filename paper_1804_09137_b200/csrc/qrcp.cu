@@ -556,8 +556,12 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   if (blocked_ok && !big.empty() && ((int)big.size() >= blocked_min || !cluster_ok)) {
     const QrcpLaunch Ls = stage(small, ar, s);
     if (!Ls.count) { launch_qrcp_blocked(big, ar, s); return; }
-    static cudaStream_t side2 = nullptr;
-    static cudaEvent_t f2 = nullptr, j2 = nullptr;
+    static cudaStream_t side2_d[kMaxDevices] = {};
+    static cudaEvent_t f2_d[kMaxDevices] = {}, j2_d[kMaxDevices] = {};
+    const int dev = current_device();
+    cudaStream_t& side2 = side2_d[dev];
+    cudaEvent_t& f2 = f2_d[dev];
+    cudaEvent_t& j2 = j2_d[dev];
     if (!side2) {
       TLRB_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
       TLRB_CUDA(cudaEventCreateWithFlags(&f2, cudaEventDisableTiming));
@@ -575,8 +579,12 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   if (!Lb.count) { run_single(Ls, s); return; }
   for (int i : big_idx) gathered[i] = 1;
   if (!Ls.count) { run_cluster(Lb, s); return; }
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  static cudaStream_t side_d[kMaxDevices] = {};
+  static cudaEvent_t fork_d[kMaxDevices] = {}, join_d[kMaxDevices] = {};
+  const int dev = current_device();
+  cudaStream_t& side = side_d[dev];
+  cudaEvent_t& fork_ev = fork_d[dev];
+  cudaEvent_t& join_ev = join_d[dev];
   if (!side) {
     TLRB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     TLRB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));

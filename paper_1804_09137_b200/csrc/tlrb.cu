@@ -29,6 +29,7 @@
 #include <cmath>
 #include <string>
 #include <chrono>
+#include <mutex>
 
 using namespace tlrb;
 
@@ -1115,6 +1116,11 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
 
 template <class F>
 int guarded(tlrb_handle* h, F&& f) {
+  // launcher caches are per device and the DescArena / workspace per handle:
+  // calls that reach the same device from several host threads take turns
+  static std::recursive_mutex dev_mu[kMaxDevices];
+  std::unique_lock<std::recursive_mutex> lk;
+  if (h && h->device >= 0 && h->device < kMaxDevices) lk = std::unique_lock<std::recursive_mutex>(dev_mu[h->device]);
   try {
     return f();
   } catch (const CudaError& e) {

@@ -393,3 +393,34 @@ def test_lookahead_potrf_identical(tb):
         assert r.returncode == 0, r.stderr[-2000:]
         out.append(r.stdout.strip().splitlines()[-1])
     assert out[0] == out[1], out
+
+
+def test_concurrent_handles_two_threads(tb):
+    """Two host threads with their own handles on the same device: calls are
+    serialised per device (launcher caches are per device), results equal
+    the serial ones bitwise."""
+    import threading
+
+    cases = [(tb.generate_locations(900, s), np.random.default_rng(s).standard_normal(900)) for s in (11, 12)]
+    p = tb.MaternParams(1.0, 0.1, 0.5)
+    serial = []
+    for locs, z in cases:
+        h = tb.Handle(locs.coords, 150)
+        serial.append(h.loglik(z, p, 1e-8)[0])
+        h.close()
+    got = [None, None]
+
+    def run(k):
+        locs, z = cases[k]
+        h = tb.Handle(locs.coords, 150)
+        vals = [h.loglik(z, p, 1e-8)[0] for _ in range(3)]
+        h.close()
+        got[k] = vals
+
+    th = [threading.Thread(target=run, args=(k,)) for k in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in (0, 1):
+        assert got[k] == [serial[k]] * 3
