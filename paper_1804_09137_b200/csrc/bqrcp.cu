@@ -361,11 +361,9 @@ __global__ void __launch_bounds__(512) bq_pick_reg_kernel(const QrcpProb* __rest
 // Unblocked Householder QR of the panel A[j:m, j:j+bb] in shared memory;
 // writes R + reflectors back to A, the explicit V (unit lower trapezoidal,
 // mr x bb, ld m) and T (bb x bb, ld b, upper) of I - V T V^T.
-__global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restrict__ probs, BqState* st,
-                                                       double* ws, size_t wsz, size_t off_v, size_t off_t,
-                                                       int j, int b) {
-  const QrcpProb P = probs[blockIdx.x];
-  if (!st[blockIdx.x].active) return;
+// P: the problem's A / lda / m / n; V: block V storage at row j (ld P.m);
+// T: the block's b x b T factor.
+__device__ void panel_qr(const QrcpProb& P, double* V, double* T, int j, int b) {
   extern __shared__ double sm[];
   const int nr = P.n - j, mr = P.m - j;
   const int bb = min(b, min(nr, mr));
@@ -431,7 +429,6 @@ __global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restric
   }
   __syncthreads();
   // write back R / reflectors, explicit V
-  double* V = ws + (size_t)blockIdx.x * wsz + off_v;
   for (int c = 0; c < bb; ++c)
     for (int r = tid; r < mr; r += blockDim.x) {
       const double x = Pn[c * mr + r];
@@ -462,11 +459,25 @@ __global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restric
     }
   }
   __syncthreads();
-  double* T = ws + (size_t)blockIdx.x * wsz + off_t;
   for (int e = tid; e < b * b; e += blockDim.x) {
     const int i = e % b, t = e / b;
     T[e] = (t < bb && i <= t) ? Ts[t * 32 + i] : 0.0;
   }
+}
+
+__global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restrict__ probs, BqState* st,
+                                                       double* ws, size_t wsz, size_t off_v, size_t off_t,
+                                                       int j, int b) {
+  if (!st[blockIdx.x].active) return;
+  panel_qr(probs[blockIdx.x], ws + (size_t)blockIdx.x * wsz + off_v, ws + (size_t)blockIdx.x * wsz + off_t, j, b);
+}
+
+// unpivoted blocked QR: the panel of block j of every problem with j < s
+__global__ void __launch_bounds__(512) bqr_panel_kernel(const BqrProb* __restrict__ probs, int j, int b) {
+  const BqrProb B = probs[blockIdx.x];
+  if (j >= B.s) return;
+  const QrcpProb P{B.A, B.lda, B.m, B.s, nullptr, nullptr, nullptr, 0.0, 0};
+  panel_qr(P, B.V + (size_t)j * B.m + j, B.T + (size_t)(j / b) * b * b, j, b);
 }
 
 // Exact residual after the block and stop test: e = ||A[j+bb:, j+bb:]||^2,
@@ -661,6 +672,87 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
     for (const BqState& x : hs) any |= x.active != 0;
     if (!any) break;
     planned = 3;
+  }
+}
+
+// ------------------------------------------------ unpivoted blocked QR
+// A (m x s) = Q R by b-column Householder panels (one CTA each, compact WY)
+// and DMMA trailing updates; R + reflectors stay in A, the explicit unit
+// lower V panels go to B.V (m x s, ld m), block q's T to B.T + q b b, and
+// B.W (>= 2 b max(s, k) doubles) is scratch.  The factored recompression's
+// stacked-factor QRs (tlrb.cu) use it; Q is never formed, it is applied.
+int qr_blocked_width(int mmax) {
+  int b = 32;
+  while (b > 8 && (size_t)mmax * b * 8 > 200 * 1024) b -= 8;
+  return b;
+}
+
+void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  int mmax = 1, smax = 0;
+  for (const BqrProb& p : probs) { mmax = std::max(mmax, p.m); smax = std::max(smax, p.s); }
+  const int b = qr_blocked_width(mmax);
+  const size_t smem_panel = (size_t)mmax * b * 8;
+  TLRB_CUDA(cudaFuncSetAttribute(bqr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_panel));
+  const BqrProb* dp = ar.put(probs, s);
+  std::vector<GemmProb> ga, gc, gd;
+  for (int j = 0; j < smax; j += b) {
+    {
+      double fl = 0;
+      for (const BqrProb& p : probs)
+        if (j < p.s) fl += 2.0 * (p.m - j) * std::min(b, p.s - j) * std::min(b, p.s - j);
+      ProfScope ps(K_QR, s, fl, 0);
+      bqr_panel_kernel<<<(unsigned)probs.size(), 512, smem_panel, s>>>(dp, j, b);
+      post_launch();
+    }
+    ga.clear(); gc.clear(); gd.clear();
+    for (const BqrProb& p : probs) {
+      if (j >= p.s) continue;
+      const int mr = p.m - j, bb = std::min(b, p.s - j), n2 = p.s - j - bb;
+      if (n2 <= 0) continue;
+      double* V = p.V + (size_t)j * p.m + j;
+      double* T = p.T + (size_t)(j / b) * b * b;
+      double* A2 = p.A + (size_t)(j + bb) * p.lda + j;
+      double* W = p.W;
+      double* W2 = p.W + (size_t)b * p.s;
+      ga.push_back({V, A2, nullptr, W, bb, n2, mr, p.m, p.lda, 0, b, 1, 0, 0, 1.0, 0.0});
+      gc.push_back({T, W, nullptr, W2, bb, n2, bb, b, b, 0, b, 1, 0, 0, 1.0, 0.0});
+      gd.push_back({V, W2, A2, A2, mr, n2, bb, p.m, b, p.lda, p.lda, 0, 0, 0, -1.0, 1.0});
+    }
+    launch_gemm(ga, ar, s);   // W = V^T A2
+    launch_gemm(gc, ar, s);   // W2 = T^T W
+    launch_gemm(gd, ar, s);   // A2 -= V W2
+  }
+}
+
+// C (m x k[p], ld ldc[p]) <- Q C for the Q of launch_qr_blocked (blocks in
+// reverse order: C_j -= V_j T_j V_j^T C_j)
+void launch_apply_q_blocked(const std::vector<BqrProb>& probs, const std::vector<double*>& C,
+                            const std::vector<int>& ldc, const std::vector<int>& k, DescArena& ar,
+                            cudaStream_t s) {
+  if (probs.empty()) return;
+  int mmax = 1, smax = 0;
+  for (const BqrProb& p : probs) { mmax = std::max(mmax, p.m); smax = std::max(smax, p.s); }
+  const int b = qr_blocked_width(mmax);
+  std::vector<GemmProb> g1, g2, g3;
+  for (int j = ((smax - 1) / b) * b; j >= 0; j -= b) {
+    g1.clear(); g2.clear(); g3.clear();
+    for (size_t q = 0; q < probs.size(); ++q) {
+      const BqrProb& p = probs[q];
+      if (j >= p.s || k[q] <= 0) continue;
+      const int mr = p.m - j, bb = std::min(b, p.s - j), kk = k[q];
+      double* V = p.V + (size_t)j * p.m + j;
+      double* T = p.T + (size_t)(j / b) * b * b;
+      double* Cj = C[q] + j;
+      double* W = p.W;
+      double* W2 = p.W + (size_t)b * kk;
+      g1.push_back({V, Cj, nullptr, W, bb, kk, mr, p.m, ldc[q], 0, b, 1, 0, 0, 1.0, 0.0});
+      g2.push_back({T, W, nullptr, W2, bb, kk, bb, b, b, 0, b, 0, 0, 0, 1.0, 0.0});
+      g3.push_back({V, W2, Cj, Cj, mr, kk, bb, p.m, b, ldc[q], ldc[q], 0, 0, 0, -1.0, 1.0});
+    }
+    launch_gemm(g1, ar, s);
+    launch_gemm(g2, ar, s);
+    launch_gemm(g3, ar, s);
   }
 }
 

@@ -191,6 +191,14 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
 void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
+// unpivoted blocked Householder QR (bqrcp.cu): R + reflectors in A (m x s),
+// explicit V panels (m x s, ld m), per-block T (b x b each), W scratch
+struct BqrProb { double* A; int lda, m, s; double* V; double* T; double* W; };
+int qr_blocked_width(int mmax);
+void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStream_t s);
+void launch_apply_q_blocked(const std::vector<BqrProb>& probs, const std::vector<double*>& C,
+                            const std::vector<int>& ldc, const std::vector<int>& k, DescArena& ar,
+                            cudaStream_t s);
 // gathered[p] = 1: columns left in place (R column jj at perm[jj]); 0: physically pivoted
 void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered, DescArena& ar,
                  cudaStream_t s);

@@ -529,13 +529,18 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   gathered.assign(probs.size(), 0);
   if (probs.empty()) return;
   static const bool no_cluster = getenv("TLRB_QRCP_NOCLUSTER") != nullptr;
-  static const int thr = getenv("TLRB_QRCP_CLUSTER_MIN") ? atoi(getenv("TLRB_QRCP_CLUSTER_MIN")) : 160;
+  static const int thr_env = getenv("TLRB_QRCP_CLUSTER_MIN") ? atoi(getenv("TLRB_QRCP_CLUSTER_MIN")) : -1;
   std::vector<QrcpProb> big, small;
   std::vector<int> big_idx;
   int mmax = 1, nmax = 1;
   for (const QrcpProb& p : probs) { mmax = std::max(mmax, p.m); nmax = std::max(nmax, p.n); }
   int CL = 0;
   const bool cluster_ok = !no_cluster && cluster_cpc(mmax, nmax, CL) > 0;
+  // "big" problems (predicted QRCP steps above thr) leave the one-CTA kernel;
+  // without the cluster kernel (nb > ~500) even modest ones go to the blocked
+  // path: the one-CTA kernel streams an nb x nb trailing matrix per pivot
+  // (C3: thr 32 -> 16.0 s vs 16.2 s at 160)
+  const int thr = thr_env >= 0 ? thr_env : (cluster_ok ? 160 : 32);
   // blocked path available for every tile size up to 2048 (the panel of b
   // columns fits in shared memory); the cluster kernel only while a matrix
   // fits in the shared memory of a 16-CTA cluster (nb <= ~500)

@@ -219,9 +219,11 @@ struct Job {
   bool dense_out;     // rank above max_rank: stored dense (L^T in Uout, ld ldu)
   uint64_t seed;      // unused (kept for descriptor stability)
   // factored recompression (compression.py:54-81): M is the K x K core,
-  // U_new = Qu u_core, V_new = Qv v_core are formed after compress_jobs
+  // U_new = Qu u_core, V_new = Qv v_core are formed after compress_jobs by
+  // applying the blocked Householder reflectors of the stacked-factor QRs
   bool factored = false;
-  double* Qu = nullptr; double* Qv = nullptr; int mu = 0, nv = 0;
+  BqrProb qu{}, qv{};
+  int mu = 0, nv = 0;
   double* Ufin = nullptr; double* Vfin = nullptr;
   long tile = -1;     // destination tile (outputs allocated once the rank is known)
   long ftile = -1;    // factored path: destination tile of Qu u_core / Qv v_core
@@ -656,7 +658,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       // factored-path launches
       std::vector<GemmProb> fx, fy, fcore;
       std::vector<CopyProb> fcp, fr;
-      std::vector<QrProb> fq;
+      std::vector<BqrProb> fq;
       std::vector<SumsqProb> fsq;
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
@@ -672,11 +674,16 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           // stacked factors Us = [U_ij, -U_ik (V_ik^T V_jk)] (mi x K), Vs = [V_ij, U_jk] (mj x K)
           double* Us = J.Y;
           double* Vs = J.Y + (size_t)mi * K;
-          double* Qu = J.Q;
-          double* Qv = J.Q + (size_t)mi * K;
-          double* Tu = J.Om;                                // qr_kernel T: 16 (K + 16) doubles
-          double* Tv = J.Om + 16 * ((size_t)K + 16);
-          double* Xs = J.Om + 32 * ((size_t)K + 16);
+          // blocked Householder QRs of the stacked factors: V panels in the
+          // Q slot, T blocks (any panel width b <= 32) and GEMM scratch in Om
+          double* Vu = J.Q;
+          double* Vv = J.Q + (size_t)mi * K;
+          const size_t TB = (size_t)((K + 7) / 8) * 1024, WS = (size_t)64 * K;
+          double* Tu = J.Om;
+          double* Tv = Tu + TB;
+          double* Wu = Tv + TB;
+          double* Wv = Wu + WS;
+          double* Xs = Wv + WS;
           double* uc = Xs + (size_t)ki * kj;
           double* vc = uc + (size_t)K * K;
           fx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, Xs, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
@@ -689,8 +696,8 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           fsq.push_back({nullptr, 0, 0, 0, S + 3});
           fsq.push_back({Vs, mj, mj, K, S + 4});
           fsq.push_back({nullptr, 0, 0, 0, S + 5});
-          fq.push_back({Us, mi, Qu, mi, Tu, mi, K});
-          fq.push_back({Vs, mj, Qv, mj, Tv, mj, K});
+          fq.push_back({Us, mi, mi, K, Vu, Tu, Wu});
+          fq.push_back({Vs, mj, mj, K, Vv, Tv, Wv});
           // R^T (lower) of both, then core = Ru Rv^T = (Ru^T)^T (Rv^T)
           fr.push_back({Us, mi, J.E, K, K, K, 1, 1.0, 1, nullptr});
           fr.push_back({Vs, mj, J.Bt, K, K, K, 1, 1.0, 1, nullptr});
@@ -702,7 +709,9 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           J.Vout = vc;
           J.ldu = J.ldv = K;
           J.factored = true;
-          J.Qu = Qu; J.Qv = Qv; J.mu = mi; J.nv = mj;
+          J.qu = fq[fq.size() - 2];
+          J.qv = fq.back();
+          J.mu = mi; J.nv = mj;
           J.ftile = (long)h->tid(i, j);
           J.seed = 0;
           jobs.push_back(J);
@@ -764,22 +773,33 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_copy(fcp, h->ar, h->stream);
       launch_gemm(fy, h->ar, h->stream);
       launch_sumsq(fsq, h->ar, h->stream);
-      launch_qr(fq, h->ar, h->stream);
+      launch_qr_blocked(fq, h->ar, h->stream);
       launch_copy(fr, h->ar, h->stream);
       launch_gemm(fcore, h->ar, h->stream);
       compress_jobs(h, jobs, acc);
       {   // U_new = Qu u_core, V_new = Qv v_core (compression.py:81)
-        std::vector<GemmProb> fu;
+        std::vector<BqrProb> fp;
+        std::vector<double*> fc;
+        std::vector<int> fld, fk;
+        std::vector<CopyProb> fin;
         for (Job& J : jobs) {
           if (!J.factored || !J.out_rank) continue;
           const int kk = J.out_rank;
           h->ensure((size_t)J.ftile, kk);
           J.Ufin = h->uptr[J.ftile];
           J.Vfin = h->vptr[J.ftile];
-          fu.push_back({J.Qu, J.Uout, nullptr, J.Ufin, J.mu, kk, J.m, J.mu, J.ldu, nb, nb, 0, 0, 0, 1.0, 0.0});
-          fu.push_back({J.Qv, J.Vout, nullptr, J.Vfin, J.nv, kk, J.n, J.nv, J.ldv, nb, nb, 0, 0, 0, 1.0, 0.0});
+          // [core factor; 0] (K x kk on top of mu - K zero rows), then Q applied in place
+          fin.push_back({J.Uout, J.ldu, J.Ufin, nb, J.m, kk, 0, 1.0, 0, nullptr});
+          fin.push_back({J.Vout, J.ldv, J.Vfin, nb, J.n, kk, 0, 1.0, 0, nullptr});
+          if (J.mu > J.m)
+            TLRB_CUDA(cudaMemset2DAsync(J.Ufin + J.m, (size_t)nb * 8, 0, (size_t)(J.mu - J.m) * 8, kk, h->stream));
+          if (J.nv > J.n)
+            TLRB_CUDA(cudaMemset2DAsync(J.Vfin + J.n, (size_t)nb * 8, 0, (size_t)(J.nv - J.n) * 8, kk, h->stream));
+          fp.push_back(J.qu); fc.push_back(J.Ufin); fld.push_back(nb); fk.push_back(kk);
+          fp.push_back(J.qv); fc.push_back(J.Vfin); fld.push_back(nb); fk.push_back(kk);
         }
-        launch_gemm(fu, h->ar, h->stream);
+        launch_copy(fin, h->ar, h->stream);
+        launch_apply_q_blocked(fp, fc, fld, fk, h->ar, h->stream);
       }
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
