@@ -117,13 +117,6 @@ struct TrsmProb {          // B <- L^-1 B (or L^-T B), L lower n x n
   int n, nrhs;
 };
 
-// ----------------------------------------------------------------------- QR
-struct QrProb {            // Householder QR of A (m x s); Q (m x s) formed explicitly
-  double* A; int lda;      // in: A; out: R (upper) + V (below diag)
-  double* Q; int ldq;
-  double* T;               // workspace: s x 16 compact-WY T factors
-  int m, s;
-};
 
 // ------------------------------------------------------------------- Jacobi
 struct JacobiProb {        // one-sided Jacobi on the columns of X (m x s)
@@ -190,7 +183,6 @@ bool have_cutlass_gemm();
 void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
-void launch_qr(const std::vector<QrProb>& probs, DescArena& ar, cudaStream_t s);
 // unpivoted blocked Householder QR (bqrcp.cu): R + reflectors in A (m x s),
 // explicit V panels (m x s, ld m), per-block T (b x b each), W scratch
 struct BqrProb { double* A; int lda, m, s; double* V; double* T; double* W; };
