@@ -45,6 +45,16 @@ double qrcp_rel_tol() {
 }
 constexpr int kPotrfBlock = 32;
 
+// Factored recompression (reference scheme: QR of the stacked factors, SVD of
+// the K x K core) for stacked ranks K <= frac min(m, n).  Measured: nb = 500
+// (C2, latency-bound steps) best at 0.1-0.15 (0.2: +2%, 0.4: +10%); nb = 760
+// (C3, throughput-bound) 15.8 s at 0.15, 13.1 s at 0.4, 11.4 s at 0.6 (the
+// slot layout caps K near nb / 2).  TLRB_FACTORED_FRAC overrides.
+double factored_frac(int nb) {
+  static const double v = getenv("TLRB_FACTORED_FRAC") ? atof(getenv("TLRB_FACTORED_FRAC")) : -1.0;
+  return v >= 0.0 ? v : (nb <= 512 ? 0.15 : 1.0);
+}
+
 struct Flops {
   double f = 0, b = 0;
   void add(double ff, double bb) { f += ff; b += bb; }
@@ -213,7 +223,7 @@ struct Job {
   int s;              // QRCP kernel hint on entry; QRCP rank r (Jacobi width) after it
   int kind;           // bit1: recompression (noise floor)
   double* M;          // slot pointers
-  double* E; double* Y; double* Q; double* Om; double* Bt; double* Vs; double* sig; double* T;
+  double* E; double* Y; double* Q; double* Om; double* Bt; double* Vs; double* F; double* sig; double* T;
   double* Uout; double* Vout; int ldu, ldv;
   int out_rank;
   bool dense_out;     // rank above max_rank: stored dense (L^T in Uout, ld ldu)
@@ -239,7 +249,8 @@ void bind_slot(tlrb_handle* h, Job& J, int slot) {
   J.Om = base + 4 * nb2;
   J.Bt = base + 5 * nb2;
   J.Vs = base + 6 * nb2;
-  J.sig = base + 7 * nb2;
+  J.F = base + 7 * nb2;     // factored path: core factors u_core, v_core
+  J.sig = base + 8 * nb2;
   J.T = J.sig + h->nb;
 }
 
@@ -648,7 +659,6 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_gemm(dy, h->ar, h->stream);
       launch_gemm(dt, h->ar, h->stream);
     }
-    static const double kFactoredFrac = getenv("TLRB_FACTORED_FRAC") ? atof(getenv("TLRB_FACTORED_FRAC")) : 0.15;
     for (size_t c0 = 0; c0 < upd.size(); c0 += h->max_jobs) {
       const size_t c1 = std::min(upd.size(), c0 + h->max_jobs);
       std::vector<Job> jobs;
@@ -669,7 +679,13 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         const int slot = (int)(q - c0);
         bind_slot(h, J, slot);
         const int K = kij + kj;
-        if (!di && !dj && !dij && K <= kFactoredFrac * std::min(mi, mj) &&
+        // the slot layout of the factored path: stacked factors (mi + mj) K in
+        // Y, their V panels in Q, T blocks + scratch + the ki x kj product in
+        // Om, the K x K core factors in F
+        const size_t nb2s = (size_t)nb * nb;
+        const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
+                          2 * ((size_t)32 * K + 1024) + 128 * (size_t)K + (size_t)ki * kj <= nb2s;
+        if (!di && !dj && !dij && fits && K <= factored_frac(nb) * std::min(mi, mj) &&
             (h->max_rank <= 0 || K <= h->max_rank)) {
           // stacked factors Us = [U_ij, -U_ik (V_ik^T V_jk)] (mi x K), Vs = [V_ij, U_jk] (mj x K)
           double* Us = J.Y;
@@ -678,14 +694,14 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           // Q slot, T blocks (any panel width b <= 32) and GEMM scratch in Om
           double* Vu = J.Q;
           double* Vv = J.Q + (size_t)mi * K;
-          const size_t TB = (size_t)((K + 7) / 8) * 1024, WS = (size_t)64 * K;
+          const size_t TB = (size_t)32 * K + 1024, WS = (size_t)64 * K;   // ceil(K/b) b^2 <= 32 K + 1024
           double* Tu = J.Om;
           double* Tv = Tu + TB;
           double* Wu = Tv + TB;
           double* Wv = Wu + WS;
-          double* Xs = Wv + WS;
-          double* uc = Xs + (size_t)ki * kj;
-          double* vc = uc + (size_t)K * K;
+          double* Xs = Wv + WS;   // ki x kj
+          double* uc = J.F;
+          double* vc = J.F + (size_t)K * K;
           fx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, Xs, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
           fcp.push_back({h->Ut(i, j), nb, Us, mi, mi, kij, 0, 1.0, 0, nullptr});
           fy.push_back({h->Ut(i, k), Xs, nullptr, Us + (size_t)mi * kij, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, -1.0, 0.0});
@@ -1203,8 +1219,8 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMalloc(&h->d_z, n * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_w, (size_t)h->t * h->nb * sizeof(double)));
     h->ar.init(64u << 20);
-    // compression workspace: 7 nb^2 + 2 nb + 16 nb doubles per job slot
-    h->slot_doubles = 7 * nb2 + 18 * (size_t)h->nb + 64;
+    // compression workspace: 8 nb^2 + 2 nb + 16 nb doubles per job slot
+    h->slot_doubles = 8 * nb2 + 18 * (size_t)h->nb + 64;
     size_t freeb = 0, totb = 0;
     TLRB_CUDA(cudaMemGetInfo(&freeb, &totb));
     // capped at 56 GB for tile grids up to 128 x 128 (fewer, larger job
