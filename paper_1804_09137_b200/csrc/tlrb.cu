@@ -72,6 +72,7 @@ struct tlrb_handle {
   cudaEvent_t ev[6];
   int64_t n = 0;
   int nb = 0, t = 0, cap = 0, max_rank = 0;
+  bool npd_seen = false;   // set by compress_jobs' readback; factor_tlr stops
   std::vector<int> off, sz;
   double* dx = nullptr;          // point coordinates in the Pts layout (a1, a2, a3)
   double* dy = nullptr;
@@ -284,7 +285,10 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   const double t_q0 = trace_on() ? now_ms() : 0;
   if (trace_on()) h->sync();
   TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  int info0 = 0;   // NPD flag of the POTRFs so far, read with the ranks (no extra sync)
+  TLRB_CUDA(cudaMemcpyAsync(&info0, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
   h->sync();
+  if (info0) h->npd_seen = true;
   const double t_q1 = trace_on() ? now_ms() : 0;
   std::vector<int> kinds(nj);
   {
@@ -539,6 +543,7 @@ bool factor_dense(tlrb_handle* h) {
 // -------------------------------------------------------- TLR factorisation
 bool factor_tlr(tlrb_handle* h, double acc) {
   const int t = h->t, nb = h->nb;
+  h->npd_seen = false;
   double* tmp = reinterpret_cast<double*>(h->ws);  // small products before the job batch
   // POTRF(k+1) only needs step k's SYRK of D(k+1): it runs on the look-ahead
   // stream while step k's recompressions run (single-GPU handles)
@@ -563,7 +568,9 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       if (r) h->work.add(nk * nk * r, 8.0 * (nk * nk / 2 + 2.0 * nk * r));
     }
     launch_trsm(tp, false, h->ar, h->stream);
-    if (check_npd(h)) return false;
+    // single GPU: the NPD flag is read with the next rank readback (no sync
+    // here); a failed POTRF only lets this step's batch run on garbage
+    if (h->dist() ? check_npd(h) : (h->npd_seen && check_npd(h))) return false;
     bcast_panel(h, k, false);
     // K5: D_j -= U_jk (V_jk^T V_jk) U_jk^T  (dense panel tile: D_j -= T_jk^T T_jk)
     {
