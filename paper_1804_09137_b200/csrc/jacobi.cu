@@ -10,7 +10,7 @@
 // exactly that.
 //
 // Parallel layout: X (m x s, column-major) lives in global memory / L2 and is
-// cut into column blocks of B.  One thread-block CLUSTER (1..8 CTAs, sized by
+// cut into column blocks of B.  One thread-block CLUSTER (1..16 CTAs, sized by
 // the matrix) owns one matrix.  A sweep is a round-robin tournament over the
 // blocks: in each round the cluster's CTAs take disjoint block pairs (I, J),
 // stage both blocks in shared memory, rotate all B x B cross column pairs
