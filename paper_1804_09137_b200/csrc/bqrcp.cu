@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(512) bq_pick_reg_kernel(const QrcpProb* __rest
 // mr x bb, ld m) and T (bb x bb, ld b, upper) of I - V T V^T.
 // P: the problem's A / lda / m / n; V: block V storage at row j (ld P.m);
 // T: the block's b x b T factor.
-__device__ void panel_qr(const QrcpProb& P, double* V, double* T, int j, int b) {
+__device__ void panel_qr(const QrcpProb& P, double* V, double* T, int j, int b, int ldt = 0) {
   extern __shared__ double sm[];
   const int nr = P.n - j, mr = P.m - j;
   const int bb = min(b, min(nr, mr));
@@ -459,9 +459,10 @@ __device__ void panel_qr(const QrcpProb& P, double* V, double* T, int j, int b) 
     }
   }
   __syncthreads();
+  if (!ldt) ldt = b;
   for (int e = tid; e < b * b; e += blockDim.x) {
     const int i = e % b, t = e / b;
-    T[e] = (t < bb && i <= t) ? Ts[t * 32 + i] : 0.0;
+    T[(size_t)t * ldt + i] = (t < bb && i <= t) ? Ts[t * 32 + i] : 0.0;
   }
 }
 
@@ -472,12 +473,28 @@ __global__ void __launch_bounds__(512) bq_panel_kernel(const QrcpProb* __restric
   panel_qr(probs[blockIdx.x], ws + (size_t)blockIdx.x * wsz + off_v, ws + (size_t)blockIdx.x * wsz + off_t, j, b);
 }
 
-// unpivoted blocked QR: the panel of block j of every problem with j < s
-__global__ void __launch_bounds__(512) bqr_panel_kernel(const BqrProb* __restrict__ probs, int j, int b) {
+// unpivoted blocked QR: the panel at column j (inside the super-block that
+// starts at J0, width SB) of every problem with j < s.  Its T goes to the
+// diagonal block of the super-block's merged T (ld SB); the rows J0..j-1 of
+// its V columns are zeroed so V of the whole super-block is explicit.
+__global__ void __launch_bounds__(512) bqr_panel_kernel(const BqrProb* __restrict__ probs, int j, int b, int J0,
+                                                        int SB) {
   const BqrProb B = probs[blockIdx.x];
   if (j >= B.s) return;
   const QrcpProb P{B.A, B.lda, B.m, B.s, nullptr, nullptr, nullptr, 0.0, 0};
-  panel_qr(P, B.V + (size_t)j * B.m + j, B.T + (size_t)(j / b) * b * b, j, b);
+  double* TJ = B.T + (size_t)(J0 / SB) * SB * SB;
+  panel_qr(P, B.V + (size_t)j * B.m + j, TJ + (size_t)(j - J0) * SB + (j - J0), j, b, SB);
+  const int bb = min(b, B.s - j);
+  for (int e = threadIdx.x; e < bb * (j - J0); e += blockDim.x) {
+    const int c = e / (j - J0), r = J0 + e % (j - J0);
+    B.V[(size_t)(j + c) * B.m + r] = 0.0;
+  }
+  // T_J is upper triangular: zero this panel's columns below its diagonal block
+  const int below = SB - (j - J0) - b;
+  for (int e = threadIdx.x; e < b * max(below, 0); e += blockDim.x) {
+    const int c = e / below, r = (j - J0) + b + e % below;
+    TJ[(size_t)((j - J0) + c) * SB + r] = 0.0;
+  }
 }
 
 // Exact residual after the block and stop test: e = ||A[j+bb:, j+bb:]||^2,
@@ -676,79 +693,129 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
 }
 
 // ------------------------------------------------ unpivoted blocked QR
-// A (m x s) = Q R by b-column Householder panels (one CTA each, compact WY)
-// and DMMA trailing updates; R + reflectors stay in A, the explicit unit
-// lower V panels go to B.V (m x s, ld m), block q's T to B.T + q b b, and
-// B.W (>= 2 b max(s, k) doubles) is scratch.  The factored recompression's
-// stacked-factor QRs (tlrb.cu) use it; Q is never formed, it is applied.
+// A (m x s) = Q R.  Panels of b columns are factored by one CTA each
+// (Householder in shared memory, compact WY); kSuper panels form a
+// super-block whose reflectors are merged into one compact-WY factor
+// I - V_J T_J V_J^T (T_J upper, SB x SB, SB = kSuper b):
+//   T_J(0:q, q) = -T_J(0:q, 0:q) (V(:, 0:q)^T V(:, q)) T_qq   (block columns q)
+// so the trailing matrix beyond a super-block and the later application of
+// Q take one rank-SB update per super-block (three DMMA GEMMs) instead of
+// kSuper rank-b ones: the m x n operand is streamed kSuper times less.
+// R + reflectors stay in A, the explicit V (zero above the diagonal within
+// each super-block) in B.V (m x s, ld m), T_J at B.T + J SB SB, and B.W
+// (>= 2 SB max(s, k) doubles) is GEMM scratch.  The factored
+// recompression's stacked-factor QRs (tlrb.cu) use it; Q is applied, never formed.
+constexpr int kSuper = 4;
+
 int qr_blocked_width(int mmax) {
   int b = 32;
   while (b > 8 && (size_t)mmax * b * 8 > 200 * 1024) b -= 8;
   return b;
 }
 
+int qr_blocked_super(int mmax) { return kSuper * qr_blocked_width(mmax); }
+
 void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
   int mmax = 1, smax = 0;
   for (const BqrProb& p : probs) { mmax = std::max(mmax, p.m); smax = std::max(smax, p.s); }
-  const int b = qr_blocked_width(mmax);
+  const int b = qr_blocked_width(mmax), SB = kSuper * b;
   const size_t smem_panel = (size_t)mmax * b * 8;
   TLRB_CUDA(cudaFuncSetAttribute(bqr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_panel));
   const BqrProb* dp = ar.put(probs, s);
   std::vector<GemmProb> ga, gc, gd;
-  for (int j = 0; j < smax; j += b) {
-    {
-      double fl = 0;
-      for (const BqrProb& p : probs)
-        if (j < p.s) fl += 2.0 * (p.m - j) * std::min(b, p.s - j) * std::min(b, p.s - j);
-      ProfScope ps(K_QR, s, fl, 0);
-      bqr_panel_kernel<<<(unsigned)probs.size(), 512, smem_panel, s>>>(dp, j, b);
-      post_launch();
+  for (int J0 = 0; J0 < smax; J0 += SB) {
+    // panels of the super-block; their updates stay inside it
+    for (int j = J0; j < std::min(smax, J0 + SB); j += b) {
+      {
+        double fl = 0;
+        for (const BqrProb& p : probs)
+          if (j < p.s) fl += 2.0 * (p.m - j) * std::min(b, p.s - j) * std::min(b, p.s - j);
+        ProfScope ps(K_QR, s, fl, 0);
+        bqr_panel_kernel<<<(unsigned)probs.size(), 512, smem_panel, s>>>(dp, j, b, J0, SB);
+        post_launch();
+      }
+      ga.clear(); gc.clear(); gd.clear();
+      for (const BqrProb& p : probs) {
+        if (j >= p.s) continue;
+        const int mr = p.m - j, bb = std::min(b, p.s - j), n2 = std::min(p.s, J0 + SB) - j - bb;
+        if (n2 <= 0) continue;
+        double* V = p.V + (size_t)j * p.m + j;
+        double* T = p.T + (size_t)(J0 / SB) * SB * SB + (size_t)(j - J0) * SB + (j - J0);
+        double* A2 = p.A + (size_t)(j + bb) * p.lda + j;
+        double* W = p.W;
+        double* W2 = p.W + (size_t)b * n2;
+        ga.push_back({V, A2, nullptr, W, bb, n2, mr, p.m, p.lda, 0, b, 1, 0, 0, 1.0, 0.0});
+        gc.push_back({T, W, nullptr, W2, bb, n2, bb, SB, b, 0, b, 1, 0, 0, 1.0, 0.0});
+        gd.push_back({V, W2, A2, A2, mr, n2, bb, p.m, b, p.lda, p.lda, 0, 0, 0, -1.0, 1.0});
+      }
+      launch_gemm(ga, ar, s);   // W = V^T A2
+      launch_gemm(gc, ar, s);   // W2 = T^T W
+      launch_gemm(gd, ar, s);   // A2 -= V W2
     }
+    // merge the super-block's panel T factors: block column q of T_J
+    for (int q = J0 + b; q < std::min(smax, J0 + SB); q += b) {
+      std::vector<GemmProb> gx, gy, gt;
+      for (const BqrProb& p : probs) {
+        if (q >= p.s) continue;
+        const int qb = q - J0, bq = std::min(b, p.s - q), mr = p.m - J0;
+        double* TJ = p.T + (size_t)(J0 / SB) * SB * SB;
+        double* VJ = p.V + (size_t)J0 * p.m + J0;      // rows J0.., explicit zeros above the panels
+        double* X = p.W;                                 // qb x bq
+        double* Y = p.W + (size_t)SB * b;                // qb x bq
+        gx.push_back({VJ, VJ + (size_t)qb * p.m, nullptr, X, qb, bq, mr, p.m, p.m, 0, qb, 1, 0, 0, 1.0, 0.0});
+        gy.push_back({X, TJ + (size_t)qb * SB + qb, nullptr, Y, qb, bq, bq, qb, SB, 0, qb, 0, 0, 0, 1.0, 0.0});
+        gt.push_back({TJ, Y, nullptr, TJ + (size_t)qb * SB, qb, bq, qb, SB, qb, 0, SB, 0, 0, 0, -1.0, 0.0});
+      }
+      launch_gemm(gx, ar, s);   // X = V(:, 0:q)^T V(:, q)
+      launch_gemm(gy, ar, s);   // Y = X T_qq
+      launch_gemm(gt, ar, s);   // T(0:q, q) = -T(0:q, 0:q) Y
+    }
+    // trailing matrix beyond the super-block: one rank-SB update
     ga.clear(); gc.clear(); gd.clear();
     for (const BqrProb& p : probs) {
-      if (j >= p.s) continue;
-      const int mr = p.m - j, bb = std::min(b, p.s - j), n2 = p.s - j - bb;
+      if (J0 >= p.s) continue;
+      const int sw = std::min(SB, p.s - J0), n2 = p.s - J0 - sw, mr = p.m - J0;
       if (n2 <= 0) continue;
-      double* V = p.V + (size_t)j * p.m + j;
-      double* T = p.T + (size_t)(j / b) * b * b;
-      double* A2 = p.A + (size_t)(j + bb) * p.lda + j;
+      double* VJ = p.V + (size_t)J0 * p.m + J0;
+      double* TJ = p.T + (size_t)(J0 / SB) * SB * SB;
+      double* A2 = p.A + (size_t)(J0 + sw) * p.lda + J0;
       double* W = p.W;
-      double* W2 = p.W + (size_t)b * p.s;
-      ga.push_back({V, A2, nullptr, W, bb, n2, mr, p.m, p.lda, 0, b, 1, 0, 0, 1.0, 0.0});
-      gc.push_back({T, W, nullptr, W2, bb, n2, bb, b, b, 0, b, 1, 0, 0, 1.0, 0.0});
-      gd.push_back({V, W2, A2, A2, mr, n2, bb, p.m, b, p.lda, p.lda, 0, 0, 0, -1.0, 1.0});
+      double* W2 = p.W + (size_t)SB * n2;
+      ga.push_back({VJ, A2, nullptr, W, sw, n2, mr, p.m, p.lda, 0, SB, 1, 0, 0, 1.0, 0.0});
+      gc.push_back({TJ, W, nullptr, W2, sw, n2, sw, SB, SB, 0, SB, 1, 0, 0, 1.0, 0.0});
+      gd.push_back({VJ, W2, A2, A2, mr, n2, sw, p.m, SB, p.lda, p.lda, 0, 0, 0, -1.0, 1.0});
     }
-    launch_gemm(ga, ar, s);   // W = V^T A2
-    launch_gemm(gc, ar, s);   // W2 = T^T W
-    launch_gemm(gd, ar, s);   // A2 -= V W2
+    launch_gemm(ga, ar, s);
+    launch_gemm(gc, ar, s);
+    launch_gemm(gd, ar, s);
   }
 }
 
-// C (m x k[p], ld ldc[p]) <- Q C for the Q of launch_qr_blocked (blocks in
-// reverse order: C_j -= V_j T_j V_j^T C_j)
+// C (m x k[p], ld ldc[p]) <- Q C for the Q of launch_qr_blocked: one rank-SB
+// update per super-block, in reverse order (C_J -= V_J T_J V_J^T C_J)
 void launch_apply_q_blocked(const std::vector<BqrProb>& probs, const std::vector<double*>& C,
                             const std::vector<int>& ldc, const std::vector<int>& k, DescArena& ar,
                             cudaStream_t s) {
   if (probs.empty()) return;
   int mmax = 1, smax = 0;
   for (const BqrProb& p : probs) { mmax = std::max(mmax, p.m); smax = std::max(smax, p.s); }
-  const int b = qr_blocked_width(mmax);
+  const int SB = qr_blocked_super(mmax);
   std::vector<GemmProb> g1, g2, g3;
-  for (int j = ((smax - 1) / b) * b; j >= 0; j -= b) {
+  for (int J0 = ((smax - 1) / SB) * SB; J0 >= 0; J0 -= SB) {
     g1.clear(); g2.clear(); g3.clear();
     for (size_t q = 0; q < probs.size(); ++q) {
       const BqrProb& p = probs[q];
-      if (j >= p.s || k[q] <= 0) continue;
-      const int mr = p.m - j, bb = std::min(b, p.s - j), kk = k[q];
-      double* V = p.V + (size_t)j * p.m + j;
-      double* T = p.T + (size_t)(j / b) * b * b;
-      double* Cj = C[q] + j;
+      if (J0 >= p.s || k[q] <= 0) continue;
+      const int mr = p.m - J0, sw = std::min(SB, p.s - J0), kk = k[q];
+      double* VJ = p.V + (size_t)J0 * p.m + J0;
+      double* TJ = p.T + (size_t)(J0 / SB) * SB * SB;
+      double* Cj = C[q] + J0;
       double* W = p.W;
-      double* W2 = p.W + (size_t)b * kk;
-      g1.push_back({V, Cj, nullptr, W, bb, kk, mr, p.m, ldc[q], 0, b, 1, 0, 0, 1.0, 0.0});
-      g2.push_back({T, W, nullptr, W2, bb, kk, bb, b, b, 0, b, 0, 0, 0, 1.0, 0.0});
-      g3.push_back({V, W2, Cj, Cj, mr, kk, bb, p.m, b, ldc[q], ldc[q], 0, 0, 0, -1.0, 1.0});
+      double* W2 = p.W + (size_t)SB * kk;
+      g1.push_back({VJ, Cj, nullptr, W, sw, kk, mr, p.m, ldc[q], 0, SB, 1, 0, 0, 1.0, 0.0});
+      g2.push_back({TJ, W, nullptr, W2, sw, kk, sw, SB, SB, 0, SB, 0, 0, 0, 1.0, 0.0});
+      g3.push_back({VJ, W2, Cj, Cj, mr, kk, sw, p.m, SB, ldc[q], ldc[q], 0, 0, 0, -1.0, 1.0});
     }
     launch_gemm(g1, ar, s);
     launch_gemm(g2, ar, s);

@@ -184,9 +184,11 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
 // unpivoted blocked Householder QR (bqrcp.cu): R + reflectors in A (m x s),
-// explicit V panels (m x s, ld m), per-block T (b x b each), W scratch
+// explicit V (m x s, ld m), merged T per super-block (SB x SB each), W scratch
+// (>= 2 SB max(s, k) doubles)
 struct BqrProb { double* A; int lda, m, s; double* V; double* T; double* W; };
 int qr_blocked_width(int mmax);
+int qr_blocked_super(int mmax);   // merged super-block width (kSuper panels)
 void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_apply_q_blocked(const std::vector<BqrProb>& probs, const std::vector<double*>& C,
                             const std::vector<int>& ldc, const std::vector<int>& k, DescArena& ar,

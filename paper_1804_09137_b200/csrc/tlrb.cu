@@ -690,23 +690,26 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         // Y, their V panels in Q, T blocks + scratch + the ki x kj product in
         // Om, the K x K core factors in F
         const size_t nb2s = (size_t)nb * nb;
+        // (merged T factors: super-blocks of <= 128 columns, <= 128 K + 128^2 each)
         const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
-                          2 * ((size_t)32 * K + 1024) + 128 * (size_t)K + (size_t)ki * kj <= nb2s;
+                          (size_t)4 * 128 * K <= nb2s &&
+                          2 * ((size_t)128 * K + 16384) + (size_t)ki * kj <= nb2s;
         if (!di && !dj && !dij && fits && K <= factored_frac(nb) * std::min(mi, mj) &&
             (h->max_rank <= 0 || K <= h->max_rank)) {
           // stacked factors Us = [U_ij, -U_ik (V_ik^T V_jk)] (mi x K), Vs = [V_ij, U_jk] (mj x K)
           double* Us = J.Y;
           double* Vs = J.Y + (size_t)mi * K;
-          // blocked Householder QRs of the stacked factors: V panels in the
-          // Q slot, T blocks (any panel width b <= 32) and GEMM scratch in Om
+          // blocked Householder QRs of the stacked factors: V in the Q slot,
+          // merged T factors in Om, GEMM scratch in F (free until the core
+          // factors land there; consumed again before the Q application)
           double* Vu = J.Q;
           double* Vv = J.Q + (size_t)mi * K;
-          const size_t TB = (size_t)32 * K + 1024, WS = (size_t)64 * K;   // ceil(K/b) b^2 <= 32 K + 1024
+          const size_t TB = (size_t)128 * K + 16384;   // ceil(K/SB) SB^2, SB <= 128
           double* Tu = J.Om;
           double* Tv = Tu + TB;
-          double* Wu = Tv + TB;
-          double* Wv = Wu + WS;
-          double* Xs = Wv + WS;   // ki x kj
+          double* Xs = Tv + TB;   // ki x kj
+          double* Wu = J.F;
+          double* Wv = J.F + nb2s / 2;
           double* uc = J.F;
           double* vc = J.F + (size_t)K * K;
           fx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, Xs, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
@@ -822,7 +825,12 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           fp.push_back(J.qv); fc.push_back(J.Vfin); fld.push_back(nb); fk.push_back(kk);
         }
         launch_copy(fin, h->ar, h->stream);
+        const double ta0 = trace_on() ? (h->sync(), now_ms()) : 0.0;
         launch_apply_q_blocked(fp, fc, fld, fk, h->ar, h->stream);
+        if (trace_on()) {
+          h->sync();
+          fprintf(stderr, "[tlrb] apply-Q %zu factors %.2f ms\n", fp.size(), now_ms() - ta0);
+        }
       }
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
