@@ -694,32 +694,41 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
 
 // ------------------------------------------------ unpivoted blocked QR
 // A (m x s) = Q R.  Panels of b columns are factored by one CTA each
-// (Householder in shared memory, compact WY); kSuper panels form a
+// (Householder in shared memory, compact WY); four panels (<= 128 columns) form a
 // super-block whose reflectors are merged into one compact-WY factor
-// I - V_J T_J V_J^T (T_J upper, SB x SB, SB = kSuper b):
+// I - V_J T_J V_J^T (T_J upper, SB x SB, SB = 4 b by default):
 //   T_J(0:q, q) = -T_J(0:q, 0:q) (V(:, 0:q)^T V(:, q)) T_qq   (block columns q)
 // so the trailing matrix beyond a super-block and the later application of
 // Q take one rank-SB update per super-block (three DMMA GEMMs) instead of
-// kSuper rank-b ones: the m x n operand is streamed kSuper times less.
+// four rank-b ones: the m x n operand is streamed four times less.
 // R + reflectors stay in A, the explicit V (zero above the diagonal within
 // each super-block) in B.V (m x s, ld m), T_J at B.T + J SB SB, and B.W
 // (>= 2 SB max(s, k) doubles) is GEMM scratch.  The factored
 // recompression's stacked-factor QRs (tlrb.cu) use it; Q is applied, never formed.
-constexpr int kSuper = 4;
+static int super_panels() {
+  static const int v = getenv("TLRB_BQR_SUPER") ? atoi(getenv("TLRB_BQR_SUPER")) : 4;
+  return v;
+}
 
 int qr_blocked_width(int mmax) {
-  int b = 32;
+  static const int b0 = getenv("TLRB_BQR_B") ? atoi(getenv("TLRB_BQR_B")) : 32;
+  int b = b0;
   while (b > 8 && (size_t)mmax * b * 8 > 200 * 1024) b -= 8;
   return b;
 }
 
-int qr_blocked_super(int mmax) { return kSuper * qr_blocked_width(mmax); }
+// super-block width: at most 128 columns (the slot layout of tlrb.cu's
+// factored path budgets merged T factors of <= 128 x 128 per super-block)
+int qr_blocked_super(int mmax) {
+  const int b = qr_blocked_width(mmax);
+  return std::max(1, std::min(super_panels(), 128 / b)) * b;
+}
 
 void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
   int mmax = 1, smax = 0;
   for (const BqrProb& p : probs) { mmax = std::max(mmax, p.m); smax = std::max(smax, p.s); }
-  const int b = qr_blocked_width(mmax), SB = kSuper * b;
+  const int b = qr_blocked_width(mmax), SB = qr_blocked_super(mmax);
   const size_t smem_panel = (size_t)mmax * b * 8;
   TLRB_CUDA(cudaFuncSetAttribute(bqr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_panel));
   const BqrProb* dp = ar.put(probs, s);

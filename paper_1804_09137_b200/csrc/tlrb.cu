@@ -799,7 +799,12 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_copy(fcp, h->ar, h->stream);
       launch_gemm(fy, h->ar, h->stream);
       launch_sumsq(fsq, h->ar, h->stream);
+      const double tq0 = trace_on() ? (h->sync(), now_ms()) : 0.0;
       launch_qr_blocked(fq, h->ar, h->stream);
+      if (trace_on()) {
+        h->sync();
+        fprintf(stderr, "[tlrb] factored-QR %zu factors %.2f ms\n", fq.size(), now_ms() - tq0);
+      }
       launch_copy(fr, h->ar, h->stream);
       launch_gemm(fcore, h->ar, h->stream);
       compress_jobs(h, jobs, acc);
