@@ -42,7 +42,13 @@ void Profiler::end(cudaStream_t s, double fl, double by) {
 void Profiler::drain() {
   static const char* tl_path = getenv("TLRB_TIMELINE");
   FILE* tl = (tl_path && epoch) ? fopen(tl_path, "a") : nullptr;
+  std::vector<Pend> keep;   // launches still running on another stream (lane2)
   for (const Pend& p : pend) {
+    if (cudaEventQuery(p.b) == cudaErrorNotReady) {
+      cudaGetLastError();
+      keep.push_back(p);
+      continue;
+    }
     float a = 0;
     if (cudaEventElapsedTime(&a, p.a, p.b) == cudaSuccess) ms[p.cls] += a;
     float t0 = 0;
@@ -51,7 +57,7 @@ void Profiler::drain() {
     pool.push_back(p.a);
     pool.push_back(p.b);
   }
-  pend.clear();
+  pend.swap(keep);
   if (tl) fclose(tl);
 }
 void Profiler::reset() {

@@ -69,6 +69,10 @@ struct tlrb_handle {
   // step's recompressions (factor_tlr)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_syrk = nullptr, ev_potrf = nullptr;
+  // factored-recompression stream: the stacked-factor QRs of a batch run
+  // beside the dense-path jobs' compression (factor_tlr)
+  cudaStream_t lane2 = nullptr;
+  cudaEvent_t ev_b = nullptr, ev_f = nullptr;
   cudaEvent_t ev[6];
   int64_t n = 0;
   int nb = 0, t = 0, cap = 0, max_rank = 0;
@@ -164,7 +168,13 @@ struct tlrb_handle {
     // the arena is reset below: descriptors queued on the look-ahead stream
     // must have been consumed too
     if (side) TLRB_CUDA(cudaStreamSynchronize(side));
-    ar.reset();
+    // descriptors still queued on lane2 keep the arena (it wraps with a
+    // device sync when full)
+    if (lane2 && cudaStreamQuery(lane2) == cudaErrorNotReady) {
+      cudaGetLastError();
+    } else {
+      ar.reset();
+    }
     if (g_prof.on) g_prof.drain();
   }
 };
@@ -263,11 +273,18 @@ void bind_slot(tlrb_handle* h, Job& J, int slot) {
 //      sigma, normalised columns (= right singular vectors in pivoted order),
 //      truncation rank k with e2 = ||residual||^2 and the noise floor
 //   4. V_k = P * columns (row un-permutation), U = E V_k (DMMA GEMM)
-void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
+void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 0) {
   const int nj = (int)jobs.size();
   if (!nj) return;
   cudaStream_t s = h->stream;
-  int* d_perm = reinterpret_cast<int*>(h->d_perm);
+  // per-job device arrays from position j0 (a batch may be compressed in parts)
+  int* d_perm = reinterpret_cast<int*>(h->d_perm) + (size_t)j0 * h->nb;
+  int* d_rank = h->d_rank + j0;
+  int* d_sweeps = h->d_sweeps + j0;
+  int* d_kind = h->d_kind + j0;
+  int* d_ok = h->d_ok + j0;
+  double* d_sums = h->d_sums + 6 * (size_t)j0;
+  double* d_aux = h->d_aux + 3 * (size_t)j0;
   std::vector<char> gathered;
   {
     std::vector<CopyProb> cp;
@@ -275,7 +292,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     for (int j = 0; j < nj; ++j) {
       Job& J = jobs[j];
       cp.push_back({J.M, J.m, J.E, J.m, J.m, J.n, 0, 1.0, 0, nullptr});
-      qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, h->d_rank + j, h->d_sums + 6 * j + 1,
+      qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, d_rank + j, d_sums + 6 * j + 1,
                     (qrcp_rel_tol() * acc) * (qrcp_rel_tol() * acc), J.s});
     }
     launch_copy(cp, h->ar, s);
@@ -284,7 +301,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
   std::vector<int> rr(nj);
   const double t_q0 = trace_on() ? now_ms() : 0;
   if (trace_on()) h->sync();
-  TLRB_CUDA(cudaMemcpyAsync(rr.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLRB_CUDA(cudaMemcpyAsync(rr.data(), d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
   int info0 = 0;   // NPD flag of the POTRFs so far, read with the ranks (no extra sync)
   TLRB_CUDA(cudaMemcpyAsync(&info0, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
   h->sync();
@@ -304,14 +321,14 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     }
     launch_copy(cp, h->ar, s);
   }
-  TLRB_CUDA(cudaMemcpyAsync(h->d_kind, h->ar.put(kinds, s), nj * sizeof(int), cudaMemcpyDeviceToDevice, s));
-  launch_aux(h->d_sums, h->d_kind, nj, h->d_aux, h->d_ok, 0.0, s);
+  TLRB_CUDA(cudaMemcpyAsync(d_kind, h->ar.put(kinds, s), nj * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  launch_aux(d_sums, d_kind, nj, d_aux, d_ok, 0.0, s);
   {
     std::vector<JacobiProb> jp;
     for (int j = 0; j < nj; ++j) {
       Job& J = jobs[j];
-      jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, h->d_aux + 3 * j, acc, h->d_rank + j,
-                    h->d_sweeps + j, J.n, J.s});
+      jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, d_aux + 3 * j, acc, d_rank + j,
+                    d_sweeps + j, J.n, J.s});
     }
     static long long* d_prof = nullptr;
     const bool prof = getenv("TLRB_JACOBI_PROF") != nullptr;
@@ -333,8 +350,8 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc) {
     }
   }
   std::vector<int> rk(nj), sw(nj);
-  TLRB_CUDA(cudaMemcpyAsync(rk.data(), h->d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
-  TLRB_CUDA(cudaMemcpyAsync(sw.data(), h->d_sweeps, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLRB_CUDA(cudaMemcpyAsync(rk.data(), d_rank, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TLRB_CUDA(cudaMemcpyAsync(sw.data(), d_sweeps, nj * sizeof(int), cudaMemcpyDeviceToHost, s));
   h->sync();
   if (trace_on()) {
     int rmax = 0, smax = 0;
@@ -677,25 +694,40 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       std::vector<CopyProb> fcp, fr;
       std::vector<BqrProb> fq;
       std::vector<SumsqProb> fsq;
-      for (size_t q = c0; q < c1; ++q) {
+      const size_t nb2s = (size_t)nb * nb;
+      // factored (reference-scheme) recompression where the slot layout holds
+      // it: stacked factors (mi + mj) K in Y, their V in Q, merged T factors
+      // (super-blocks <= 128 columns: <= 128 K + 128^2 each) + the ki x kj
+      // product in Om, GEMM scratch and the K x K core factors in F
+      auto use_factored = [&](int i, int j) {
+        const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], kij = h->rank[h->tid(i, j)];
+        const int mi = h->sz[i], mj = h->sz[j], K = kij + kj;
+        const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
+                          (size_t)4 * 128 * K <= nb2s &&
+                          2 * ((size_t)128 * K + 16384) + (size_t)ki * kj <= nb2s;
+        return !h->dn(i, k) && !h->dn(j, k) && !h->dn(i, j) && fits &&
+               K <= factored_frac(nb) * std::min(mi, mj) && (h->max_rank <= 0 || K <= h->max_rank);
+      };
+      // dense-path jobs first (slots 0..nd-1), factored ones after them
+      std::vector<size_t> order;
+      std::vector<char> isf(c1 - c0);
+      for (size_t q = c0; q < c1; ++q) isf[q - c0] = use_factored(upd[q].first, upd[q].second);
+      for (size_t q = c0; q < c1; ++q) if (!isf[q - c0]) order.push_back(q);
+      const int nd = (int)order.size();
+      for (size_t q = c0; q < c1; ++q) if (isf[q - c0]) order.push_back(q);
+      std::vector<int> posq(c1 - c0);
+      for (size_t pos = 0; pos < order.size(); ++pos) {
+        const size_t q = order[pos];
+        posq[q - c0] = (int)pos;
         const int i = upd[q].first, j = upd[q].second;
         const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], kij = h->rank[h->tid(i, j)];
         const bool di = h->dn(i, k), dj = h->dn(j, k), dij = h->dn(i, j);
         const int mi = h->sz[i], mj = h->sz[j], mk = h->sz[k];
         Job J{};
-        const int slot = (int)(q - c0);
+        const int slot = (int)pos;
         bind_slot(h, J, slot);
         const int K = kij + kj;
-        // the slot layout of the factored path: stacked factors (mi + mj) K in
-        // Y, their V panels in Q, T blocks + scratch + the ki x kj product in
-        // Om, the K x K core factors in F
-        const size_t nb2s = (size_t)nb * nb;
-        // (merged T factors: super-blocks of <= 128 columns, <= 128 K + 128^2 each)
-        const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
-                          (size_t)4 * 128 * K <= nb2s &&
-                          2 * ((size_t)128 * K + 16384) + (size_t)ki * kj <= nb2s;
-        if (!di && !dj && !dij && fits && K <= factored_frac(nb) * std::min(mi, mj) &&
-            (h->max_rank <= 0 || K <= h->max_rank)) {
+        if (isf[q - c0]) {
           // stacked factors Us = [U_ij, -U_ik (V_ik^T V_jk)] (mi x K), Vs = [V_ij, U_jk] (mj x K)
           double* Us = J.Y;
           double* Vs = J.Y + (size_t)mi * K;
@@ -786,6 +818,13 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         }
         jobs.push_back(J);
       }
+      const int nf = (int)jobs.size() - nd;
+      const bool two = nd > 0 && nf > 0;
+      cudaStream_t fs = two ? h->lane2 : h->stream;   // factored-path prep stream
+      if (two) {
+        TLRB_CUDA(cudaEventRecord(h->ev_b, h->stream));
+        TLRB_CUDA(cudaStreamWaitEvent(h->lane2, h->ev_b, 0));
+      }
       launch_gemm(gx, h->ar, h->stream);
       launch_gemm(gy, h->ar, h->stream);
       launch_gemm(gm, h->ar, h->stream);
@@ -794,20 +833,26 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       // noise-floor norms (Y = U2 exists now; the tile's old factors are
       // only overwritten at the end of compress_jobs)
       launch_sumsq(sq, h->ar, h->stream);
-      // factored path: stacked factors, two Householder QRs, K x K core
-      launch_gemm(fx, h->ar, h->stream);
-      launch_copy(fcp, h->ar, h->stream);
-      launch_gemm(fy, h->ar, h->stream);
-      launch_sumsq(fsq, h->ar, h->stream);
-      const double tq0 = trace_on() ? (h->sync(), now_ms()) : 0.0;
-      launch_qr_blocked(fq, h->ar, h->stream);
-      if (trace_on()) {
-        h->sync();
-        fprintf(stderr, "[tlrb] factored-QR %zu factors %.2f ms\n", fq.size(), now_ms() - tq0);
+      // factored path: stacked factors, two Householder QRs, K x K core; on
+      // lane2 beside the dense jobs' QRCP / Jacobi when the batch has both
+      launch_gemm(fx, h->ar, fs);
+      launch_copy(fcp, h->ar, fs);
+      launch_gemm(fy, h->ar, fs);
+      launch_sumsq(fsq, h->ar, fs);
+      launch_qr_blocked(fq, h->ar, fs);
+      launch_copy(fr, h->ar, fs);
+      launch_gemm(fcore, h->ar, fs);
+      if (two) {
+        TLRB_CUDA(cudaEventRecord(h->ev_f, h->lane2));
+        std::vector<Job> jd(jobs.begin(), jobs.begin() + nd), jf(jobs.begin() + nd, jobs.end());
+        compress_jobs(h, jd, acc, 0);
+        TLRB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_f, 0));
+        compress_jobs(h, jf, acc, nd);
+        std::copy(jd.begin(), jd.end(), jobs.begin());
+        std::copy(jf.begin(), jf.end(), jobs.begin() + nd);
+      } else {
+        compress_jobs(h, jobs, acc);
       }
-      launch_copy(fr, h->ar, h->stream);
-      launch_gemm(fcore, h->ar, h->stream);
-      compress_jobs(h, jobs, acc);
       {   // U_new = Qu u_core, V_new = Qv v_core (compression.py:81)
         std::vector<BqrProb> fp;
         std::vector<double*> fc;
@@ -842,7 +887,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         const double ki = h->dn(i, k) ? h->sz[k] : h->rank[h->tid(i, k)];
         const double kj = h->dn(j, k) ? h->sz[k] : h->rank[h->tid(j, k)];
         const double kij = h->dn(i, j) ? h->sz[j] : h->rank[h->tid(i, j)];
-        const Job& J = jobs[q - c0];
+        const Job& J = jobs[posq[q - c0]];
         const double kn = J.dense_out ? h->sz[j] : J.out_rank;
         const double K = kij + kj, Kh = std::min<double>(K, h->nb), nbd = h->sz[i];
         h->work.add(4.0 * nbd * ki * kj + 2.0 * (4.0 * nbd * K * Kh - 4.0 / 3.0 * Kh * Kh * Kh) +
@@ -1207,6 +1252,9 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaSetDevice(device));
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    TLRB_CUDA(cudaStreamCreateWithFlags(&h->lane2, cudaStreamNonBlocking));
+    TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+    TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_f, cudaEventDisableTiming));
     TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_syrk, cudaEventDisableTiming));
     TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_potrf, cudaEventDisableTiming));
     for (auto& e : h->ev) TLRB_CUDA(cudaEventCreate(&e));
@@ -1335,6 +1383,9 @@ void tlrb_destroy(tlrb_handle* h) {
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->lane2) cudaStreamDestroy(h->lane2);
+  if (h->ev_b) cudaEventDestroy(h->ev_b);
+  if (h->ev_f) cudaEventDestroy(h->ev_f);
   if (h->ev_syrk) cudaEventDestroy(h->ev_syrk);
   if (h->ev_potrf) cudaEventDestroy(h->ev_potrf);
   delete h;
