@@ -699,14 +699,23 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       // it: stacked factors (mi + mj) K in Y, their V in Q, merged T factors
       // (super-blocks <= 128 columns: <= 128 K + 128^2 each) + the ki x kj
       // product in Om, GEMM scratch and the K x K core factors in F
+      // rank of the update's low-rank form L_ik L_jk^T = Y W^T: the product
+      // of two low-rank panel tiles keeps kj columns, and one dense (A13)
+      // panel tile times a low-rank one keeps the low-rank one's; two dense
+      // panel tiles: no low-rank form (-1)
+      auto upd_rank = [&](int i, int j) {
+        const bool di = h->dn(i, k), dj = h->dn(j, k);
+        return di && dj ? -1 : dj ? h->rank[h->tid(i, k)] : h->rank[h->tid(j, k)];
+      };
       auto use_factored = [&](int i, int j) {
+        const int ku = upd_rank(i, j);
+        if (ku < 0 || h->dn(i, j)) return false;
         const int ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], kij = h->rank[h->tid(i, j)];
-        const int mi = h->sz[i], mj = h->sz[j], K = kij + kj;
+        const int mi = h->sz[i], mj = h->sz[j], K = kij + ku;
         const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
                           (size_t)4 * 128 * K <= nb2s &&
                           2 * ((size_t)128 * K + 16384) + (size_t)ki * kj <= nb2s;
-        return !h->dn(i, k) && !h->dn(j, k) && !h->dn(i, j) && fits &&
-               K <= factored_frac(nb) * std::min(mi, mj) && (h->max_rank <= 0 || K <= h->max_rank);
+        return fits && K <= factored_frac(nb) * std::min(mi, mj) && (h->max_rank <= 0 || K <= h->max_rank);
       };
       // dense-path jobs first (slots 0..nd-1), factored ones after them
       std::vector<size_t> order;
@@ -726,9 +735,13 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         Job J{};
         const int slot = (int)pos;
         bind_slot(h, J, slot);
-        const int K = kij + kj;
         if (isf[q - c0]) {
-          // stacked factors Us = [U_ij, -U_ik (V_ik^T V_jk)] (mi x K), Vs = [V_ij, U_jk] (mj x K)
+          // stacked factors Us = [U_ij, -Y] (mi x K), Vs = [V_ij, W] (mj x K), L_ik L_jk^T = Y W^T:
+          //   both panel tiles low-rank: Y = U_ik (V_ik^T V_jk), W = U_jk
+          //   L_jk dense (stored L_jk^T): Y = U_ik,            W = L_jk V_ik
+          //   L_ik dense (stored L_ik^T): Y = L_ik V_jk,       W = U_jk
+          const int ku = upd_rank(i, j);
+          const int K = kij + ku;
           double* Us = J.Y;
           double* Vs = J.Y + (size_t)mi * K;
           // blocked Householder QRs of the stacked factors: V in the Q slot,
@@ -744,11 +757,19 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           double* Wv = J.F + nb2s / 2;
           double* uc = J.F;
           double* vc = J.F + (size_t)K * K;
-          fx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, Xs, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
           fcp.push_back({h->Ut(i, j), nb, Us, mi, mi, kij, 0, 1.0, 0, nullptr});
-          fy.push_back({h->Ut(i, k), Xs, nullptr, Us + (size_t)mi * kij, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, -1.0, 0.0});
           fcp.push_back({h->Vt(i, j), nb, Vs, mj, mj, kij, 0, 1.0, 0, nullptr});
-          fcp.push_back({h->Ut(j, k), nb, Vs + (size_t)mj * kij, mj, mj, kj, 0, 1.0, 0, nullptr});
+          if (!di && !dj) {
+            fx.push_back({h->Vt(i, k), h->Vt(j, k), nullptr, Xs, ki, kj, mk, nb, nb, ki, ki, 1, 0, 0, 1.0, 0.0});
+            fy.push_back({h->Ut(i, k), Xs, nullptr, Us + (size_t)mi * kij, mi, kj, ki, nb, ki, mi, mi, 0, 0, 0, -1.0, 0.0});
+            fcp.push_back({h->Ut(j, k), nb, Vs + (size_t)mj * kij, mj, mj, kj, 0, 1.0, 0, nullptr});
+          } else if (dj) {
+            fcp.push_back({h->Ut(i, k), nb, Us + (size_t)mi * kij, mi, mi, ki, 0, -1.0, 0, nullptr});
+            fy.push_back({h->Ut(j, k), h->Vt(i, k), nullptr, Vs + (size_t)mj * kij, mj, ki, mk, nb, nb, mj, mj, 1, 0, 0, 1.0, 0.0});
+          } else {
+            fy.push_back({h->Ut(i, k), h->Vt(j, k), nullptr, Us + (size_t)mi * kij, mi, kj, mk, nb, nb, mi, mi, 1, 0, 0, -1.0, 0.0});
+            fcp.push_back({h->Ut(j, k), nb, Vs + (size_t)mj * kij, mj, mj, kj, 0, 1.0, 0, nullptr});
+          }
           double* S = h->d_sums + 6 * slot;
           fsq.push_back({Us, mi, mi, K, S + 2});
           fsq.push_back({nullptr, 0, 0, 0, S + 3});
