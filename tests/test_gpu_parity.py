@@ -424,3 +424,19 @@ def test_concurrent_handles_two_threads(tb):
         t.join()
     for k in (0, 1):
         assert got[k] == [serial[k]] * 3
+
+
+def test_max_rank_c3p_factored_with_dense_operands(tb):
+    """C3p (nb = 760) with a storage cap of 200: its offset-1 tiles (rank 258)
+    go dense (A13), so the updates that multiply a dense panel tile by a
+    low-rank one take the factored path with the low-rank operand's rank;
+    the likelihood stays within the TLR tolerance of the reference's
+    (uncapped) C3p value."""
+    e, locs, z = _patch(tb, "C3p")
+    acc = 1e-7
+    cfg = tb.LikelihoodConfig(mode="tlr", accuracy=acc, nb=e["nb"], max_rank=200)
+    ll = tb.log_likelihood(locs, z, tb.MaternParams(*e["theta"]), cfg)
+    ref = e["modes"]["tlr:1e-07"]["ll"]
+    assert abs(ll - ref) <= max(1e-8, 10 * acc) * abs(ref)
+    rm = tb.api._handle_for(locs.coords, e["nb"], 200, 1).rank_map()
+    assert (np.tril(rm, -1) == -1).any()
