@@ -550,8 +550,15 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
     hmax = std::max(hmax, p.hint);
   }
   // block width: the panel (mmax x b doubles) must fit in shared memory
-  int b = 32;
+  static const int b_env = getenv("TLRB_BQ_B") ? atoi(getenv("TLRB_BQ_B")) : 32;
+  int b = b_env;
   while (b > 8 && (size_t)mmax * b * 8 > 200 * 1024) b -= 8;
+  // beyond the register pick (n <= 512) prefer a block whose l x n sketch
+  // fits in shared memory: the pick then never re-reads Y from L2
+  // (nb = 760: b = 24, C3 10.0 -> 9.6 s)
+  if (!getenv("TLRB_BQ_B") && nmax > 512)
+    for (int bt = b; bt >= 8; bt -= 8)
+      if (((size_t)(bt + 8) * nmax + nmax + bt + 8) * 8 <= 200 * 1024) { b = bt; break; }
   const int l = b + 8;
   // per-problem workspace: Y (l x nmax) | V (mmax x b) | T (b x b) | W (b x nmax) | W2 (b x nmax)
   const size_t off_v = (size_t)l * nmax, off_t = off_v + (size_t)mmax * b, off_w = off_t + (size_t)b * b,
