@@ -440,3 +440,23 @@ def test_max_rank_c3p_factored_with_dense_operands(tb):
     assert abs(ll - ref) <= max(1e-8, 10 * acc) * abs(ref)
     rm = tb.api._handle_for(locs.coords, e["nb"], 200, 1).rank_map()
     assert (np.tril(rm, -1) == -1).any()
+
+
+@pytest.mark.parametrize("n,nb,theta,acc", [
+    (777, 100, (1.3, 0.05, 2.5), 1e-9),          # ragged last tile, closed-form nu = 5/2
+    (500, 64, (0.7, 0.2, 1.5, 0.05), 1e-6),      # nu = 3/2 with a nugget
+    (300, 400, (1.0, 0.1, 0.5), 1e-7),           # nb > n: one tile
+    (640, 128, (1.0, 0.08, 0.8), 1e-3),          # loose threshold, general K_nu
+])
+def test_edge_configs_vs_oracle(tb, n, nb, theta, acc):
+    """Edge configurations against the CPU oracle (pinned to the reference):
+    dense within 1e-10, TLR within max(1e-8, 10 acc) of the oracle's TLR."""
+    locs = tb.generate_locations(n, 21)
+    z = np.random.default_rng(22).standard_normal(n)
+    p = tb.MaternParams(*theta)
+    want_d = orc.log_likelihood(locs.coords, z, theta, nb, None)[0]
+    want_t = orc.log_likelihood(locs.coords, z, theta, nb, acc)[0]
+    got_d = tb.log_likelihood(locs, z, p, tb.LikelihoodConfig(nb=nb, nugget=p.nugget))
+    got_t = tb.log_likelihood(locs, z, p, tb.LikelihoodConfig(mode="tlr", accuracy=acc, nb=nb, nugget=p.nugget))
+    assert abs(got_d - want_d) <= 1e-10 * abs(want_d)
+    assert abs(got_t - want_t) <= max(1e-8, 10 * acc) * abs(want_t)
