@@ -19,6 +19,12 @@
  *   linalg.NotPositiveDefiniteError linalg.py:20-33 -> TLRB_ERR_NPD + tlrb_last_error
  *
  * Return codes of every int-returning call.
+ *
+ * Threading: a handle lives on one device; calls that reach the same device
+ * (from any host thread, on any handle) are serialised inside the library,
+ * calls on different devices run concurrently.  Distributed handles
+ * (tlrb_create_dist) hold an NCCL communicator: every rank makes the same
+ * sequence of calls.
  */
 #ifndef TLRB200_H
 #define TLRB200_H
