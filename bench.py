@@ -19,6 +19,12 @@ N > 1: one process per GPU, tiles 2D block-cyclic over a P x Q grid with NCCL
 panel broadcasts (tlrb_create_dist); value = max-over-ranks device time of the
 shared evaluation (strong scaling).
 
+JSON extras: `roofline` (dominant kernel class, measured live; `traffic`
+from profiles/ncu_traffic.json), `step_roofline` (whole
+evaluation, algorithmic flops / bytes against the measured peaks), `kernels`
+(per-class breakdown of one profiled warm-up step), `variants` (dense /
+1e-7 / 1e-5 with their parity), `parity`, `phases_ms`, `work`.
+
 `--impl reference` times the CPU oracle port (oracle/, a restatement of the
 reference pinned to its goldens) on the host cores with a bounded stratified
 sample per step (oracle/cpu_baseline.py).
