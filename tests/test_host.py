@@ -99,3 +99,27 @@ def test_no_forbidden_batched_copies():
     bad = ["Memcpy" + "Batch", "Memcpy3D" + "Batch"]
     for p in (ROOT / "paper_1804_09137_b200" / "csrc").glob("*"):
         assert not any(b in p.read_text() for b in bad), p
+
+
+def test_recorded_bench_line_contract():
+    """The committed bench line (profiles/r01_bench_c2.json, produced on a
+    B200 by bench.py) carries every key of the driver contract."""
+    import json
+    from conftest import ROOT
+
+    d = json.loads((ROOT / "profiles" / "r01_bench_c2.json").read_text())
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline",
+              "cpu_baseline", "clocks"):
+        assert k in d, k
+    assert d["higher_is_better"] is False and d["dtype"] == "f64" and d["n_gpus"] == 1
+    assert "workload" in d["config"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert d["roofline"]["traffic"] and d["roofline"]["bound"] in ("hbm", "tensor")
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in d["cpu_baseline"], k
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert d["gpu_launches"] > 0 and d["parity"]["rel"] <= d["parity"]["tol"]
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
