@@ -63,8 +63,10 @@ typedef struct tlrb_stats {
 
 /* Create a handle for n locations (xy: n x 2, row-major, like
  * LocationSet.coords).  nb: tile size (min(nb, n) is used), ngpus: 1 in this
- * build, max_rank: <=0 means uncapped, device: CUDA ordinal.  Locations stay
- * resident on the device across evaluations.  *err receives a TLRB_* code. */
+ * build, max_rank: <=0 means uncapped, device: CUDA ordinal.  min(nb, n)
+ * above 2048 is refused (TLRB_ERR_ARG): the compression kernels stage at most
+ * 2048 rows per column.  Locations stay resident on the device across
+ * evaluations.  *err receives a TLRB_* code. */
 tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
                          int32_t max_rank, int32_t device, int32_t* err);
 void tlrb_destroy(tlrb_handle* h);

@@ -44,6 +44,7 @@ double qrcp_rel_tol() {
   return v;
 }
 constexpr int kPotrfBlock = 32;
+constexpr int kMaxTile = 2048;   // largest supported tile size (rows staged per column)
 
 // Factored recompression (reference scheme: QR of the stacked factors, SVD of
 // the K x K core) for stacked ranks K <= frac min(m, n).  Measured: nb = 500
@@ -1263,7 +1264,9 @@ extern "C" {
 tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus, int32_t max_rank,
                          int32_t device, int32_t* err) {
   if (err) *err = TLRB_OK;
-  if (!xy || n < 1 || nb < 1 || ngpus != 1) {
+  // the compression kernels stage at most 2048 rows per column (QRCP / Jacobi
+  // register tiles of 64 doubles per lane): larger tiles are refused
+  if (!xy || n < 1 || nb < 1 || ngpus != 1 || std::min<int64_t>(nb, n) > kMaxTile) {
     if (err) *err = TLRB_ERR_ARG;
     return nullptr;
   }

@@ -123,3 +123,11 @@ def test_recorded_bench_line_contract():
         assert k in d["e2e"], k
     assert d["gpu_launches"] > 0 and d["parity"]["rel"] <= d["parity"]["tol"]
     assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_tile_size_limit_before_device(tb):
+    """Tiles above 2048 rows are refused before any device work (ValueError),
+    instead of being compressed on truncated columns."""
+    xy = np.random.default_rng(0).random((3000, 2))
+    with pytest.raises(ValueError):
+        tb.Handle(xy, 2500)
