@@ -460,3 +460,21 @@ def test_edge_configs_vs_oracle(tb, n, nb, theta, acc):
     got_t = tb.log_likelihood(locs, z, p, tb.LikelihoodConfig(mode="tlr", accuracy=acc, nb=nb, nugget=p.nugget))
     assert abs(got_d - want_d) <= 1e-10 * abs(want_d)
     assert abs(got_t - want_t) <= max(1e-8, 10 * acc) * abs(want_t)
+
+
+@pytest.mark.parametrize("name", ["C3p"])   # C4p (cond ~4e8) amplifies any TLR error: 1e-5 there
+def test_kriging_patch_tlr_vs_dense(tb, name):
+    """Kriging on the large-tile patches (nb = 760 / 1000: factored and dense
+    recompressions, blocked QRCP): TLR(1e-9) predictions within the
+    reference's own bound max|TLR - dense| <= 1e-6 (test_predict.py:55-60,
+    there at acc 1e-9 as here)."""
+    e, locs, z = _patch(tb, name)
+    p = tb.MaternParams(*e["theta"])
+    rng = np.random.default_rng(2)
+    idx = np.sort(rng.choice(len(locs), size=50, replace=False))
+    mask = np.zeros(len(locs), bool)
+    mask[idx] = True
+    kn, un = tb.LocationSet(locs.coords[~mask]), tb.LocationSet(locs.coords[mask])
+    dense = tb.predict(tb.PredictionProblem(kn, z[~mask], un, p, nb=e["nb"]))
+    tlr = tb.predict(tb.PredictionProblem(kn, z[~mask], un, p, "tlr", 1e-9, e["nb"]))
+    assert np.max(np.abs(tlr - dense)) <= 1e-6
