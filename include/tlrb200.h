@@ -40,6 +40,11 @@ extern "C" {
 #define TLRB_ERR_ARG 2     /* invalid argument (shape, theta, accuracy) */
 #define TLRB_ERR_CUDA 3    /* CUDA / NCCL / out-of-memory */
 
+/* communicator backends of tlrb_create_group */
+#define TLRB_BACKEND_AUTO 0      /* NCCL when the devices are distinct, else loopback */
+#define TLRB_BACKEND_NCCL 1      /* NCCL over NVLink / NVSwitch, one rank per device */
+#define TLRB_BACKEND_LOOPBACK 2  /* in-process: host rendezvous + stream-ordered device copies */
+
 typedef struct tlrb_handle tlrb_handle;
 
 /* Per-evaluation statistics (phase times measured with CUDA events on the
@@ -59,31 +64,59 @@ typedef struct tlrb_stats {
   double mean_rank;
   int32_t sketch_retries; /* compression sketches that had to be enlarged */
   int32_t jacobi_max_sweeps;
+  double t_roof_ms;       /* sum over ops of max(F / P64, B / BW) (tlrb_set_peaks) */
+  int64_t arena_peak_bytes; /* high-water mark of this rank's tile factor arena */
+  int64_t panel_peak_bytes; /* largest received panel (distributed handles) */
 } tlrb_stats;
 
 /* Create a handle for n locations (xy: n x 2, row-major, like
- * LocationSet.coords).  nb: tile size (min(nb, n) is used), ngpus: 1 in this
- * build, max_rank: <=0 means uncapped, device: CUDA ordinal.  min(nb, n)
- * above 2048 is refused (TLRB_ERR_ARG): the compression kernels stage at most
- * 2048 rows per column.  Locations stay resident on the device across
- * evaluations.  *err receives a TLRB_* code. */
+ * LocationSet.coords).  nb: tile size (min(nb, n) is used), max_rank: <=0
+ * means uncapped, device: CUDA ordinal.  ngpus > 1: this one handle drives
+ * devices device .. device + ngpus - 1 from the calling process (2D
+ * block-cyclic tiles, as tlrb_create_dist, NCCL between the devices, one host
+ * thread per device inside each call) — the replacement for
+ * LikelihoodConfig(ngpus=G) in a single-process caller such as mle_fit.
+ * min(nb, n) above 2048 is refused (TLRB_ERR_ARG): the compression kernels
+ * stage at most 2048 rows per column.  Locations stay resident on the device
+ * across evaluations.  *err receives a TLRB_* code. */
 tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
                          int32_t max_rank, int32_t device, int32_t* err);
 void tlrb_destroy(tlrb_handle* h);
 
 /* Multi-GPU (one process per GPU): 2D block-cyclic tile distribution over a
  * P x Q process grid (P * Q == world), tile (i, j) on rank (i mod P) * Q +
- * (j mod Q).  Per panel k: the owner of D_k factors it and broadcasts L_kk,
- * owners of the panel tiles solve them and broadcast {U_ik, V_ik} (or the
- * dense tile), owners of D_j / (i, j) apply their updates; ranks are
- * all-reduced after every panel; log-det is all-reduced; the triangular
- * solves reduce/broadcast one tile vector per step.  All collectives are NCCL
- * on the handle's stream.  rank 0 creates the id with tlrb_nccl_unique_id
- * (128 bytes) and shares it out of band (e.g. torch.distributed). */
+ * (j mod Q); rank r is in process row r / Q and process column r mod Q, with
+ * a communicator for each.  Per panel k: the owner of D_k
+ * factors it and broadcasts L_kk down its process column; the panel owners
+ * solve their tiles; one world all-reduce carries the NPD flag and the
+ * panel's ranks; the panel goes out packed, along process rows (tiles (i, k)
+ * to the owners of row i) then down process columns (tiles (j, k) to the
+ * owners of column j); owners of D_j / (i, j) apply their updates and the
+ * received panel is dropped, so a rank stores its own tiles plus one panel.
+ * log-det is all-reduced; the triangular solves reduce a tile vector along a
+ * process row (column) and broadcast it down a column (row) per step.  All
+ * collectives run on the handle's stream.  rank 0 creates the id with
+ * tlrb_nccl_unique_id (128 bytes) and shares it out of band (e.g.
+ * torch.distributed). */
 int32_t tlrb_nccl_unique_id(char* out, int32_t len);
 tlrb_handle* tlrb_create_dist(const double* xy, int64_t n, int32_t nb, int32_t max_rank,
                               int32_t device, int32_t rank, int32_t world, int32_t P,
                               int32_t Q, const char* nccl_id, int32_t* err);
+
+/* The same 2D block-cyclic schedule with `world` ranks inside this process,
+ * rank r on devices[r] (devices may repeat), driven by one host thread per
+ * rank within each call.  backend TLRB_BACKEND_LOOPBACK runs the collectives
+ * as host rendezvous + stream-ordered device copies (no kernel waits on
+ * another rank), so W logical ranks can share one GPU: the multi-GPU path is
+ * executed and checked on one B200.  Every tlrb_* call on the returned handle
+ * runs on all ranks; outputs come from rank 0. */
+tlrb_handle* tlrb_create_group(const double* xy, int64_t n, int32_t nb, int32_t max_rank,
+                               const int32_t* devices, int32_t world, int32_t P, int32_t Q,
+                               int32_t backend, int32_t* err);
+/* Ranks behind a handle (1 for a single-GPU or one-process-per-GPU handle). */
+int32_t tlrb_group_size(tlrb_handle* h);
+/* The last evaluation's statistics of one rank of a group handle. */
+int32_t tlrb_member_stats(tlrb_handle* h, int32_t member, tlrb_stats* st);
 
 /* Distance metric of the handle's locations.  sphere_radius == 0: Euclidean
  * (the default after create); > 0: great-circle (haversine) distance on a
@@ -168,6 +201,13 @@ int32_t tlrb_profile_enable(int32_t on);
 int32_t tlrb_profile_mask(uint32_t mask);
 int32_t tlrb_profile_read(int32_t cls, char* name, int32_t len, double* ms, double* flops,
                           double* bytes, int64_t* launches);
+/* Busy time (ms) of one class since enable: the union of its launches'
+ * [start, end] intervals, so launches of one class overlapping on several
+ * streams count once (cls = -1: union over every class). */
+int32_t tlrb_profile_busy(int32_t cls, double* busy_ms);
+/* Peaks behind tlrb_stats.t_roof_ms (default 35.5 TFLOP/s FP64 DMMA,
+ * 6449.7 GB/s HBM: the measured B200 figures). */
+int32_t tlrb_set_peaks(double fp64_tflops, double hbm_gbs);
 
 #ifdef __cplusplus
 }

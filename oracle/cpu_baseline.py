@@ -39,7 +39,7 @@ def _t(fn, *a, reps: int = 2):
     return best, out
 
 
-def _warm(nb: int) -> None:
+def warm(nb: int) -> None:
     """Spin up the BLAS / LAPACK thread pool and workspaces once."""
     a = np.random.default_rng(0).standard_normal((nb, nb))
     sla.svd(a, full_matrices=False, check_finite=False, lapack_driver="gesdd")
@@ -57,7 +57,7 @@ def estimate_eval_seconds(xy, z, theta, nb, acc, pair_budget: int = 14) -> tuple
     b = orc.tile_bounds(n, nb)
     t = len(b)
     mid = t // 2
-    _warm(nb)
+    warm(nb)
 
     def tile(i, j):
         return orc.matern_block(xy[b[i][0]:b[i][1]], xy[b[j][0]:b[j][1]], theta)
@@ -118,6 +118,26 @@ def estimate_eval_seconds(xy, z, theta, nb, acc, pair_budget: int = 14) -> tuple
             f"{len(samples)} recompressions over (d1,d2) offset pairs, extrapolated to "
             f"{t * (t - 1) // 2} tiles and {t * (t - 1) * (t - 2) // 6} updates")
     return total, desc
+
+
+def calibration() -> dict:
+    """The estimator against full timed runs of the unmodified reference: the
+    C3 TLR(1e-7) golden run (tests/golden/c3_tlr.json, one evaluation on the
+    build container's host cores) and the estimator on the same host
+    (profiles/r02_reference_calibration.json)."""
+    from pathlib import Path
+    import json
+    root = Path(__file__).resolve().parents[1]
+    out = {}
+    g = root / "tests" / "golden" / "c3_tlr.json"
+    if g.exists():
+        d = json.loads(g.read_text())["C3"]
+        out["full_reference_c3_tlr_s"] = d.get("seconds")
+        out["full_reference_host"] = d.get("host", "build container, 8 cores")
+    c = root / "profiles" / "r02_reference_calibration.json"
+    if c.exists():
+        out.update(json.loads(c.read_text()))
+    return out
 
 
 def host_threads() -> int:

@@ -15,6 +15,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libtlrb200.so"
 
 TLRB_OK, TLRB_ERR_NPD, TLRB_ERR_ARG, TLRB_ERR_CUDA = 0, 1, 2, 3
+TLRB_BACKEND_AUTO, TLRB_BACKEND_NCCL, TLRB_BACKEND_LOOPBACK = 0, 1, 2
 
 
 class TlrbStats(C.Structure):
@@ -33,6 +34,9 @@ class TlrbStats(C.Structure):
         ("mean_rank", C.c_double),
         ("sketch_retries", C.c_int32),
         ("jacobi_max_sweeps", C.c_int32),
+        ("t_roof_ms", C.c_double),
+        ("arena_peak_bytes", C.c_int64),
+        ("panel_peak_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -74,6 +78,12 @@ SIGNATURES = [
     ("tlrb_profile_mask", C.c_int32, [C.c_uint32]),
     ("tlrb_profile_read", C.c_int32, [C.c_int32, C.c_char_p, C.c_int32, _DP, _DP, _DP,
                                       C.POINTER(C.c_int64)]),
+    ("tlrb_profile_busy", C.c_int32, [C.c_int32, _DP]),
+    ("tlrb_create_group", C.c_void_p, [_DP, C.c_int64, C.c_int32, C.c_int32, _IP, C.c_int32, C.c_int32,
+                                       C.c_int32, C.c_int32, _IP]),
+    ("tlrb_group_size", C.c_int32, [C.c_void_p]),
+    ("tlrb_member_stats", C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p]),
+    ("tlrb_set_peaks", C.c_int32, [C.c_double, C.c_double]),
 ]
 
 
@@ -117,9 +127,18 @@ def profile_read() -> dict:
         v = np.zeros(3)
         cnt = C.c_int64(0)
         lib.tlrb_profile_read(cls, name, 64, dptr(v[0:]), dptr(v[1:]), dptr(v[2:]), C.byref(cnt))
+        busy = np.zeros(1)
+        lib.tlrb_profile_busy(cls, dptr(busy))
         out[name.value.decode()] = {"ms": float(v[0]), "flops": float(v[1]), "bytes": float(v[2]),
-                                    "launches": int(cnt.value)}
+                                    "launches": int(cnt.value), "busy_ms": float(busy[0])}
     return out
+
+
+def profile_busy_all() -> float:
+    """Union of every profiled launch interval since profile_enable() (ms)."""
+    busy = np.zeros(1)
+    load().tlrb_profile_busy(-1, dptr(busy))
+    return float(busy[0])
 
 
 def dptr(a: np.ndarray):

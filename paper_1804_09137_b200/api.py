@@ -173,11 +173,22 @@ class LikelihoodConfig:
             raise ValueError("tlr mode requires an accuracy threshold")
         if self.mode == "tlr" and not (0.0 < self.accuracy < 1.0):
             raise ValueError(f"accuracy must lie in (0, 1), got {self.accuracy}")
+        for lo, hi in self.bounds:   # stats.py:60-62
+            if not (0.0 < lo < hi):
+                raise ValueError(f"invalid bounds ({lo}, {hi})")
+        if self.ngpus < 1:
+            raise ValueError(f"ngpus must be >= 1, got {self.ngpus}")
 
     def tile_size(self) -> int:
         if self.nb is not None:
             return self.nb
         return DEFAULT_NB_DENSE if self.mode == "dense" else DEFAULT_NB_TLR
+
+    def label(self) -> str:
+        """Canonical mode label (stats.py:68-69, 266-270): "dense" or e.g. "tlr:1e-5"."""
+        if self.mode == "dense":
+            return "dense"
+        return "tlr:" + f"{self.accuracy:g}".replace("e-0", "e-").replace("e+0", "e+")
 
 
 # --------------------------------------------------------------------------
@@ -186,16 +197,27 @@ class Handle:
     arenas reused across evaluations (one MLE run = one handle)."""
 
     def __init__(self, coords: np.ndarray, nb: int, max_rank: int = 0, ngpus: int = 1,
-                 device: int = 0, dist: tuple | None = None, radius: float = 0.0):
+                 device: int = 0, dist: tuple | None = None, radius: float = 0.0,
+                 group: tuple | None = None):
         """dist = (rank, world, P, Q, nccl_id_bytes): 2D block-cyclic multi-GPU
-        handle (one process per GPU); see `distributed_handle`.  radius > 0:
-        great-circle metric on that sphere, coords = (lon, lat) degrees."""
+        handle (one process per GPU); see `distributed_handle`.  ngpus > 1:
+        one handle driving devices device .. device + ngpus - 1 from this
+        process.  group = (devices, P, Q, backend): the same schedule with
+        len(devices) ranks in this process (devices may repeat; backend
+        _lib.TLRB_BACKEND_LOOPBACK runs several ranks on one GPU), see
+        `group_handle`.  radius > 0: great-circle metric on that sphere,
+        coords = (lon, lat) degrees."""
         self.lib = _lib.load()
         xy = np.ascontiguousarray(coords, dtype=np.float64)
         self.n = xy.shape[0]
         self.nb = int(min(nb, self.n))
         err = np.zeros(1, np.int32)
-        if dist is None:
+        if group is not None:
+            devs, P, Q, backend = group
+            d = np.ascontiguousarray(devs, dtype=np.int32)
+            self.h = self.lib.tlrb_create_group(dptr(xy), self.n, self.nb, int(max_rank or 0), iptr(d),
+                                                int(d.size), int(P), int(Q), int(backend), iptr(err))
+        elif dist is None:
             self.h = self.lib.tlrb_create(dptr(xy), self.n, self.nb, int(ngpus), int(max_rank or 0),
                                           int(device), iptr(err))
         else:
@@ -288,6 +310,18 @@ class Handle:
             self._raise(rc)
         return out
 
+    @property
+    def world(self) -> int:
+        """Ranks behind this handle (1 unless it is a group handle)."""
+        return int(self.lib.tlrb_group_size(self.h))
+
+    def member_stats(self, member: int) -> dict:
+        """The last evaluation's statistics of one rank of a group handle."""
+        st = TlrbStats()
+        if self.lib.tlrb_member_stats(self.h, int(member), C.byref(st)):
+            raise ValueError(f"no member {member}")
+        return st.as_dict()
+
     def rank_map(self) -> np.ndarray:
         t = np.zeros(1, np.int32)
         self.lib.tlrb_rank_map(self.h, None, 0, iptr(t))
@@ -330,7 +364,24 @@ def distributed_handle(coords, nb: int, max_rank: int = 0, P: int | None = None,
     return Handle(coords, nb, max_rank, device=device, dist=(rank, world, P, Q, nid), radius=radius)
 
 
-_HANDLES: dict = {}
+def group_handle(coords, nb: int, world: int, max_rank: int = 0, devices=None, P: int | None = None,
+                 Q: int | None = None, backend: int | None = None, radius: float = 0.0) -> Handle:
+    """`world` ranks of the 2D block-cyclic schedule inside this process, one
+    host thread each per call (tlrb_create_group).  devices defaults to
+    [0] * world with the loopback backend: the multi-GPU path executed on one
+    GPU (its collectives are host rendezvous + stream-ordered device copies,
+    no kernel waits on another rank)."""
+    from .dist import grid_shape
+    if P is None or Q is None:
+        P, Q = grid_shape(world)
+    devices = [0] * world if devices is None else list(devices)
+    if backend is None:
+        backend = _lib.TLRB_BACKEND_AUTO
+    return Handle(coords, nb, max_rank, group=(devices, P, Q, backend), radius=radius)
+
+
+_HANDLES: dict = {}   # insertion-ordered: least recently used first
+_MAX_HANDLES = 2      # each handle owns arenas sized from free HBM: keep few alive
 
 
 def _local_device() -> int:
@@ -339,19 +390,49 @@ def _local_device() -> int:
     return int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def _handle_key(coords: np.ndarray, nb: int, max_rank, ngpus, radius: float = 0.0):
+    return (coords.__array_interface__["data"][0], coords.shape[0], int(nb), int(max_rank or 0),
+            int(ngpus or 1), float(radius))
+
+
 def _handle_for(coords: np.ndarray, nb: int, max_rank, ngpus, radius: float = 0.0) -> Handle:
-    key = (coords.__array_interface__["data"][0], coords.shape[0], int(nb), int(max_rank or 0), ngpus,
-           radius)
-    h = _HANDLES.get(key)
+    """Cached handle for (coords, nb, max_rank, ngpus, metric): an MLE run
+    reuses one handle.  A small LRU: evicted handles are closed at once, so
+    their device arenas are released before the next handle sizes its own."""
+    key = _handle_key(coords, nb, max_rank, ngpus, radius)
+    h = _HANDLES.pop(key, None)
     if h is None or h[0] is not coords:
-        if len(_HANDLES) > 8:
-            _HANDLES.clear()
-        if ngpus and ngpus > 1:   # one process per GPU under torch.distributed
+        if h is not None:
+            h[1].close()
+        while len(_HANDLES) >= _MAX_HANDLES:
+            old = _HANDLES.pop(next(iter(_HANDLES)))
+            old[1].close()
+        if ngpus and ngpus > 1 and _torch_distributed_world() > 1:
+            # one process per GPU under torch.distributed: NCCL ranks
             h = (coords, distributed_handle(coords, nb, max_rank or 0, radius=radius))
         else:
-            h = (coords, Handle(coords, nb, max_rank or 0, device=_local_device(), radius=radius))
-        _HANDLES[key] = h
+            # one process driving ngpus devices (one host thread per device)
+            h = (coords, Handle(coords, nb, max_rank or 0, ngpus=int(ngpus or 1),
+                                device=_local_device(), radius=radius))
+    _HANDLES[key] = h
     return h[1]
+
+
+def close_handles() -> None:
+    """Release every cached device handle (their arenas go back to the GPU)."""
+    while _HANDLES:
+        _, h = _HANDLES.popitem()
+        h[1].close()
+
+
+def _torch_distributed_world() -> int:
+    try:
+        import torch.distributed as tdist
+        if tdist.is_available() and tdist.is_initialized():
+            return tdist.get_world_size()
+    except ImportError:
+        pass
+    return 1
 
 
 def _coords_of(locs) -> np.ndarray:

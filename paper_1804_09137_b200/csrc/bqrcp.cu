@@ -564,17 +564,12 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
   const size_t off_v = (size_t)l * nmax, off_t = off_v + (size_t)mmax * b, off_w = off_t + (size_t)b * b,
                off_w2 = off_w + (size_t)b * nmax;
   const size_t wsz = (off_w2 + (size_t)b * nmax + 31) & ~(size_t)31;
-  static double* ws_d[kMaxDevices] = {};
-  static size_t ws_cap_d[kMaxDevices] = {};
-  static BqState* st_d[kMaxDevices] = {};
-  static int st_cap_d[kMaxDevices] = {};
-  static double* omega_d[kMaxDevices] = {};
-  const int dev = current_device();
-  double*& ws = ws_d[dev];
-  size_t& ws_cap = ws_cap_d[dev];
-  BqState*& st = st_d[dev];
-  int& st_cap = st_cap_d[dev];
-  double*& omega = omega_d[dev];
+  LaunchCtx& cx = launch_ctx();
+  double*& ws = cx.bq_ws;
+  size_t& ws_cap = cx.bq_ws_cap;
+  BqState* st = static_cast<BqState*>(cx.bq_st);
+  int& st_cap = cx.bq_st_cap;
+  double*& omega = cx.bq_omega;
   constexpr int kOmegaCols = 2048;
   if ((size_t)np * wsz > ws_cap) {
     if (ws) TLRB_CUDA(cudaFree(ws));
@@ -585,6 +580,7 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
     if (st) TLRB_CUDA(cudaFree(st));
     st_cap = np;
     TLRB_CUDA(cudaMalloc(&st, st_cap * sizeof(BqState)));
+    cx.bq_st = st;
   }
   if (!omega) {   // fixed Gaussian test matrix (kMaxL x 2048, ld kMaxL), splitmix64 + Box-Muller
     std::vector<double> h((size_t)kMaxL * kOmegaCols);
@@ -615,8 +611,8 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
   const size_t smem_pick = ((stage_y ? (size_t)l * nmax : 0) + nmax + l) * 8;
   const size_t smem_panel = (size_t)mmax * b * 8;
   auto pick = stage_y ? bq_pick_kernel<true> : bq_pick_kernel<false>;
-  TLRB_CUDA(cudaFuncSetAttribute(pick, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pick));
-  TLRB_CUDA(cudaFuncSetAttribute(bq_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_panel));
+  allow_smem(pick, smem_pick);
+  allow_smem(bq_panel_kernel, smem_panel);
   const int kmax_all = std::min(mmax, nmax);
   int planned = (std::min(hmax, kmax_all) + b - 1) / b + 2;
   int it = 0;
@@ -737,7 +733,7 @@ void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStr
   for (const BqrProb& p : probs) { mmax = std::max(mmax, p.m); smax = std::max(smax, p.s); }
   const int b = qr_blocked_width(mmax), SB = qr_blocked_super(mmax);
   const size_t smem_panel = (size_t)mmax * b * 8;
-  TLRB_CUDA(cudaFuncSetAttribute(bqr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_panel));
+  allow_smem(bqr_panel_kernel, smem_panel);
   const BqrProb* dp = ar.put(probs, s);
   std::vector<GemmProb> ga, gc, gd;
   for (int J0 = 0; J0 < smax; J0 += SB) {

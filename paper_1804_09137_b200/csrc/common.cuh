@@ -6,10 +6,12 @@
 #include <vector>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 
 namespace tlrb {
 
-extern int64_t g_launches;  // kernels launched by this library (process-wide)
+extern std::atomic<int64_t> g_launches;  // kernels launched by this library (process-wide)
 
 #define TLRB_CUDA(call)                                                        \
   do {                                                                         \
@@ -42,15 +44,19 @@ struct Profiler {
   double ms[K_NCLASS] = {}, flops[K_NCLASS] = {}, bytes[K_NCLASS] = {};
   int64_t count[K_NCLASS] = {};
   struct Pend { int cls; cudaEvent_t a, b; cudaStream_t s; double fl; };
-  cudaEvent_t epoch = nullptr;   // TLRB_TIMELINE=path: per-launch (class, start, end) dump
+  cudaEvent_t epoch = nullptr;   // time origin (reset): per-launch intervals, TLRB_TIMELINE dump
   std::vector<Pend> pend;
+  // per-class launch intervals [start, end] in ms since `epoch`: the union is
+  // the class's busy time (launches of one class on several streams overlap)
+  std::vector<std::pair<float, float>> iv[K_NCLASS];
+  double busy_ms(int cls);   // cls < 0: union over every class
   std::vector<cudaEvent_t> pool;
-  int open_cls = -1;
-  cudaEvent_t open_ev = nullptr;
+  std::mutex mu;             // launches may come from several host threads (group handles)
   cudaEvent_t get();
-  void begin(int cls, cudaStream_t s);
-  void end(cudaStream_t s, double fl, double by);
+  cudaEvent_t begin(cudaStream_t s);
+  void end(int cls, cudaEvent_t a, cudaStream_t s, double fl, double by);
   void add_work(int cls, double fl, double by) {
+    std::lock_guard<std::mutex> lk(mu);
     if ((mask >> cls) & 1u) { flops[cls] += fl; bytes[cls] += by; }
   }
   void drain();   // after a stream synchronisation
@@ -58,12 +64,11 @@ struct Profiler {
 };
 extern Profiler g_prof;
 struct ProfScope {   // RAII: times one launch of class cls
-  cudaStream_t s; double fl, by; bool act;
-  ProfScope(int cls, cudaStream_t st, double f = 0, double b = 0)
-      : s(st), fl(f), by(b), act(g_prof.on && ((g_prof.mask >> cls) & 1u)) {
-    if (act) g_prof.begin(cls, st);
+  int cls; cudaStream_t s; double fl, by; cudaEvent_t a = nullptr;
+  ProfScope(int c, cudaStream_t st, double f = 0, double b = 0) : cls(c), s(st), fl(f), by(b) {
+    if (g_prof.on && ((g_prof.mask >> cls) & 1u)) a = g_prof.begin(st);
   }
-  ~ProfScope() { if (act) g_prof.end(s, fl, by); }
+  ~ProfScope() { if (a) g_prof.end(cls, a, s, fl, by); }
 };
 
 // clock64 phase counters inside the QRCP / Jacobi kernels (TLRB_QRCP_PROF /
@@ -143,15 +148,54 @@ struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid
 
 // Device-resident descriptor staging (pinned host ring -> device), reset at
 // stream synchronisation points.
-// Launcher-side caches (side streams, events, scratch) are kept per device:
-// a process may drive handles on several GPUs (calls on one device are
-// serialised by the C ABI, tlrb.cu).
 constexpr int kMaxDevices = 16;
 inline int current_device() {
   int d = 0;
   TLRB_CUDA(cudaGetDevice(&d));
   if (d < 0 || d >= kMaxDevices) throw CudaError(cudaErrorInvalidDevice, "device index >= 16", __FILE__, __LINE__);
   return d;
+}
+
+// Launcher-side caches (side streams, events, blocked-QRCP scratch) belong to
+// a launch context: one per handle, selected for the calling thread by the C
+// ABI (tlrb.cu guarded()).  Handles — including several logical ranks on one
+// device — therefore never share launcher state and may run concurrently.
+struct LaunchCtx {
+  int device = -1;
+  // bqrcp.cu
+  double* bq_ws = nullptr; size_t bq_ws_cap = 0;
+  void* bq_st = nullptr; int bq_st_cap = 0;
+  double* bq_omega = nullptr;
+  // jacobi.cu
+  cudaStream_t jac_side[4] = {}; cudaEvent_t jac_fork = nullptr, jac_join[4] = {};
+  // qrcp.cu
+  cudaStream_t q_side = nullptr, q_side2 = nullptr;
+  cudaEvent_t q_fork = nullptr, q_join = nullptr, q_f2 = nullptr, q_j2 = nullptr;
+  void release();   // frees everything above (on `device`)
+};
+constexpr int kMaxCtx = 256;
+int acquire_ctx();             // a free context slot (throws when all are taken)
+void release_ctx(int slot);    // frees its resources and the slot
+void set_thread_ctx(int slot); // the calling thread's launches use this context
+LaunchCtx& launch_ctx();        // the calling thread's context
+
+// Dynamic shared memory of a kernel: the attribute is raised to the device's
+// opt-in maximum (not to this launch's need), so launches of one kernel from
+// several host threads (group handles) never lower it under one another.
+template <class K>
+void allow_smem(K kern, size_t need) {
+  static const int optin = [] {
+    int v = 0;
+    TLRB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, current_device()));
+    return v;
+  }();
+  cudaFuncAttributes fa{};
+  TLRB_CUDA(cudaFuncGetAttributes(&fa, kern));
+  const int room = optin - (int)fa.sharedSizeBytes;   // static shared memory counts against the opt-in limit
+  if ((int64_t)need > room)
+    throw CudaError(cudaErrorInvalidValue, "kernel shared memory above the device limit", __FILE__, __LINE__);
+  if (fa.maxDynamicSharedSizeBytes < room)
+    TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, room));
 }
 
 class DescArena {

@@ -11,7 +11,11 @@
 // tiles; BK = 16; operands staged global -> registers -> shared memory with a
 // two-stage ping-pong so the next K slab loads while DMMAs run.
 #include "common.cuh"
+#include <chrono>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 namespace tlrb {
 
@@ -161,7 +165,56 @@ void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, 
   post_launch();
 }
 
+// TLRB_GEMM_STATS=1 (diagnostic, serialising): per launch, the stream is
+// synchronised around the call and the time is split over the launch's
+// problems by flops; buckets (m, n, k rounded up to powers of two, large-plain
+// flag) are printed at exit.  Used to aim the GEMM work.
+namespace {
+struct GemmStats {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int, int>, std::tuple<int64_t, double, double>> b;   // count, flops, ms
+  ~GemmStats() {
+    if (b.empty()) return;
+    fprintf(stderr, "[gemm-stats] m n k large count gflop ms tflops\n");
+    for (auto& [k, v] : b)
+      fprintf(stderr, "[gemm-stats] %d %d %d %d %lld %.3f %.3f %.2f\n", std::get<0>(k), std::get<1>(k),
+              std::get<2>(k), std::get<3>(k), (long long)std::get<0>(v), std::get<1>(v) / 1e9, std::get<2>(v),
+              std::get<2>(v) > 0 ? std::get<1>(v) / (std::get<2>(v) * 1e-3) / 1e12 : 0.0);
+  }
+};
+GemmStats g_gstats;
+int p2(int x) {
+  int r = 1;
+  while (r < x) r <<= 1;
+  return r;
+}
+}  // namespace
+
+void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
+
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
+  static const bool stats = getenv("TLRB_GEMM_STATS") != nullptr;
+  if (!stats || probs.empty()) return launch_gemm_impl(probs, ar, s);
+  TLRB_CUDA(cudaStreamSynchronize(s));
+  const auto t0 = std::chrono::steady_clock::now();
+  launch_gemm_impl(probs, ar, s);
+  TLRB_CUDA(cudaStreamSynchronize(s));
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  double tot = 0;
+  for (const GemmProb& p : probs) tot += 2.0 * p.m * p.n * p.k;
+  std::lock_guard<std::mutex> lk(g_gstats.mu);
+  for (const GemmProb& p : probs) {
+    if (p.m <= 0 || p.n <= 0) continue;
+    const double f = 2.0 * p.m * p.n * p.k;
+    const int large = !(p.lower_only || p.active || p.m < 64 || p.n < 64);
+    auto& v = g_gstats.b[{p2(p.m), p2(p.n), p2(std::max(1, p.k)), large}];
+    std::get<0>(v) += 1;
+    std::get<1>(v) += f;
+    std::get<2>(v) += tot > 0 ? ms * f / tot : 0.0;
+  }
+}
+
+void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
   // large plain problems go to the CUTLASS grouped DMMA kernel (gemm_cutlass.cu);
   // lower-only, flagged and skinny ones stay here (TLRB_GEMM_CUTLASS=0: all here)

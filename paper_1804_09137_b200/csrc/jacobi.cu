@@ -693,12 +693,10 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
   // independent problem groups run concurrently: the largest-cluster group
   // on the caller's stream, the others on side streams forked/joined with
   // events (they would otherwise serialise behind each other)
-  static cudaStream_t side_d[kMaxDevices][4] = {};
-  static cudaEvent_t fork_d[kMaxDevices] = {}, join_d[kMaxDevices][4] = {};
-  const int dev = current_device();
-  cudaStream_t* side = side_d[dev];
-  cudaEvent_t& fork_ev = fork_d[dev];
-  cudaEvent_t* join_ev = join_d[dev];
+  LaunchCtx& cx = launch_ctx();
+  cudaStream_t* side = cx.jac_side;
+  cudaEvent_t& fork_ev = cx.jac_fork;
+  cudaEvent_t* join_ev = cx.jac_join;
   if (!fork_ev) {
     TLRB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
     for (int i = 0; i < 4; ++i) {
@@ -755,7 +753,7 @@ void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStre
     const int bmax = k1_768 ? (v768 == 2 ? 12 : 8) : gm <= 768 ? 14 : gm <= 1024 ? 8 : 4;
     if (Bg > bmax) Bg = bmax;
     const size_t smem = std::max((size_t)2 * Bg * MP * 8, (size_t)smax * 20 + 64);
-    TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    allow_smem(kern, smem);
     if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     double by = 0;
     for (const JacobiProb& p : groups[g]) by += 8.0 * 3.0 * p.m * p.s;

@@ -5,16 +5,17 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 namespace tlrb {
 
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
 Profiler g_prof;
 const char* kclass_name[K_NCLASS] = {"gen_tiles", "dgemm_vbatch", "trsm_vbatch", "potrf_block",
                                      "qr_householder", "jacobi_svd", "sumsq", "copy", "unused",
                                      "reduce", "cross_gemv"};
 
-cudaEvent_t Profiler::get() {
+cudaEvent_t Profiler::get() {   // caller holds mu
   if (pool.empty()) {
     cudaEvent_t e;
     TLRB_CUDA(cudaEventCreate(&e));
@@ -24,22 +25,23 @@ cudaEvent_t Profiler::get() {
   pool.pop_back();
   return e;
 }
-void Profiler::begin(int cls, cudaStream_t s) {
-  open_cls = cls;
-  open_ev = get();
-  TLRB_CUDA(cudaEventRecord(open_ev, s));
+cudaEvent_t Profiler::begin(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(mu);
+  cudaEvent_t a = get();
+  TLRB_CUDA(cudaEventRecord(a, s));
+  return a;
 }
-void Profiler::end(cudaStream_t s, double fl, double by) {
-  if (open_cls < 0) return;
+void Profiler::end(int cls, cudaEvent_t a, cudaStream_t s, double fl, double by) {
+  std::lock_guard<std::mutex> lk(mu);
   cudaEvent_t b = get();
   TLRB_CUDA(cudaEventRecord(b, s));
-  pend.push_back({open_cls, open_ev, b, s, fl});
-  flops[open_cls] += fl;
-  bytes[open_cls] += by;
-  count[open_cls] += 1;
-  open_cls = -1;
+  pend.push_back({cls, a, b, s, fl});
+  flops[cls] += fl;
+  bytes[cls] += by;
+  count[cls] += 1;
 }
 void Profiler::drain() {
+  std::lock_guard<std::mutex> lk(mu);
   static const char* tl_path = getenv("TLRB_TIMELINE");
   FILE* tl = (tl_path && epoch) ? fopen(tl_path, "a") : nullptr;
   std::vector<Pend> keep;   // launches still running on another stream (lane2)
@@ -52,8 +54,10 @@ void Profiler::drain() {
     float a = 0;
     if (cudaEventElapsedTime(&a, p.a, p.b) == cudaSuccess) ms[p.cls] += a;
     float t0 = 0;
-    if (tl && cudaEventElapsedTime(&t0, epoch, p.a) == cudaSuccess)
-      fprintf(tl, "%s %.4f %.4f %p %.6g\n", kclass_name[p.cls], t0, t0 + a, (void*)p.s, p.fl);
+    if (epoch && cudaEventElapsedTime(&t0, epoch, p.a) == cudaSuccess) {
+      iv[p.cls].push_back({t0, t0 + a});
+      if (tl) fprintf(tl, "%s %.4f %.4f %p %.6g\n", kclass_name[p.cls], t0, t0 + a, (void*)p.s, p.fl);
+    }
     pool.push_back(p.a);
     pool.push_back(p.b);
   }
@@ -62,11 +66,79 @@ void Profiler::drain() {
 }
 void Profiler::reset() {
   drain();
-  if (getenv("TLRB_TIMELINE")) {   // new time origin
-    if (!epoch) TLRB_CUDA(cudaEventCreate(&epoch));
-    TLRB_CUDA(cudaEventRecord(epoch, 0));
+  // new time origin for the per-launch intervals (GPU timestamps are global
+  // across streams)
+  if (!epoch) TLRB_CUDA(cudaEventCreate(&epoch));
+  TLRB_CUDA(cudaEventRecord(epoch, 0));
+  TLRB_CUDA(cudaEventSynchronize(epoch));
+  for (int i = 0; i < K_NCLASS; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0, iv[i].clear();
+}
+double Profiler::busy_ms(int cls) {
+  drain();
+  std::lock_guard<std::mutex> lk(mu);
+  std::vector<std::pair<float, float>> all;
+  for (int c = 0; c < K_NCLASS; ++c)
+    if (cls < 0 || c == cls) all.insert(all.end(), iv[c].begin(), iv[c].end());
+  std::sort(all.begin(), all.end());
+  double tot = 0, a = -1e30, b = -1e30;
+  for (const auto& x : all) {
+    if (x.first > b) { if (b > a) tot += b - a; a = x.first; b = x.second; }
+    else b = std::max(b, (double)x.second);
   }
-  for (int i = 0; i < K_NCLASS; ++i) ms[i] = flops[i] = bytes[i] = 0, count[i] = 0;
+  if (b > a) tot += b - a;
+  return tot;
+}
+
+// ------------------------------------------------------- launch contexts
+namespace {
+LaunchCtx g_ctx[kMaxCtx];
+bool g_ctx_used[kMaxCtx] = {};
+std::mutex g_ctx_mu;
+thread_local int t_ctx = 0;   // slot 0: threads outside any handle call
+}  // namespace
+
+void LaunchCtx::release() {
+  if (device >= 0) cudaSetDevice(device);
+  if (bq_ws) cudaFree(bq_ws);
+  if (bq_st) cudaFree(bq_st);
+  if (bq_omega) cudaFree(bq_omega);
+  for (int i = 0; i < 4; ++i) {
+    if (jac_side[i]) cudaStreamDestroy(jac_side[i]);
+    if (jac_join[i]) cudaEventDestroy(jac_join[i]);
+  }
+  if (jac_fork) cudaEventDestroy(jac_fork);
+  if (q_side) cudaStreamDestroy(q_side);
+  if (q_side2) cudaStreamDestroy(q_side2);
+  for (cudaEvent_t e : {q_fork, q_join, q_f2, q_j2})
+    if (e) cudaEventDestroy(e);
+  *this = LaunchCtx{};
+}
+
+int acquire_ctx() {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  for (int i = 1; i < kMaxCtx; ++i)
+    if (!g_ctx_used[i]) {
+      g_ctx_used[i] = true;
+      g_ctx[i] = LaunchCtx{};
+      g_ctx[i].device = current_device();
+      return i;
+    }
+  throw CudaError(cudaErrorLaunchOutOfResources, "too many live handles (launch contexts)", __FILE__, __LINE__);
+}
+
+void release_ctx(int slot) {
+  if (slot <= 0 || slot >= kMaxCtx) return;
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  g_ctx[slot].release();
+  g_ctx_used[slot] = false;
+}
+
+void set_thread_ctx(int slot) { t_ctx = (slot > 0 && slot < kMaxCtx) ? slot : 0; }
+
+LaunchCtx& launch_ctx() {
+  LaunchCtx& c = g_ctx[t_ctx];
+  if (c.device < 0) c.device = current_device();
+  return c;
 }
 
 void DescArena::init(size_t bytes) {

@@ -481,7 +481,7 @@ static void run_cluster(const QrcpLaunch& L, cudaStream_t s) {
   const int cpc = cluster_cpc(L.mmax, L.nmax, CL);
   const size_t smem = ((size_t)cpc * L.mmax + (size_t)L.mmax + cpc) * 8;
   auto kern = L.mmax <= 512 ? qrcp_cluster_kernel<16, 1024> : qrcp_cluster_kernel<32, 512>;
-  TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  allow_smem(kern, smem);
   if (CL > 8) TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   ProfScope ps(K_QR, s, L.fl, L.by);
   cudaLaunchConfig_t cfg = {};
@@ -514,7 +514,7 @@ static void run_single(const QrcpLaunch& L, cudaStream_t s) {
   auto kern = L.mmax <= 512 ? qrcp_kernel<16, 1024> : L.mmax <= 1024 ? qrcp_kernel<32, 512>
                                                      : qrcp_kernel<64, 256>;
   const int nt = L.mmax <= 512 ? 1024 : L.mmax <= 1024 ? 512 : 256;
-  TLRB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  allow_smem(kern, smem);
   ProfScope ps(K_QR, s, L.fl, L.by);
   kern<<<(unsigned)L.count, nt, smem, s>>>(L.dp);
   post_launch();
@@ -561,12 +561,10 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   if (blocked_ok && !big.empty() && ((int)big.size() >= blocked_min || !cluster_ok)) {
     const QrcpLaunch Ls = stage(small, ar, s);
     if (!Ls.count) { launch_qrcp_blocked(big, ar, s); return; }
-    static cudaStream_t side2_d[kMaxDevices] = {};
-    static cudaEvent_t f2_d[kMaxDevices] = {}, j2_d[kMaxDevices] = {};
-    const int dev = current_device();
-    cudaStream_t& side2 = side2_d[dev];
-    cudaEvent_t& f2 = f2_d[dev];
-    cudaEvent_t& j2 = j2_d[dev];
+    LaunchCtx& cx = launch_ctx();
+    cudaStream_t& side2 = cx.q_side2;
+    cudaEvent_t& f2 = cx.q_f2;
+    cudaEvent_t& j2 = cx.q_j2;
     if (!side2) {
       TLRB_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
       TLRB_CUDA(cudaEventCreateWithFlags(&f2, cudaEventDisableTiming));
@@ -584,12 +582,10 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
   if (!Lb.count) { run_single(Ls, s); return; }
   for (int i : big_idx) gathered[i] = 1;
   if (!Ls.count) { run_cluster(Lb, s); return; }
-  static cudaStream_t side_d[kMaxDevices] = {};
-  static cudaEvent_t fork_d[kMaxDevices] = {}, join_d[kMaxDevices] = {};
-  const int dev = current_device();
-  cudaStream_t& side = side_d[dev];
-  cudaEvent_t& fork_ev = fork_d[dev];
-  cudaEvent_t& join_ev = join_d[dev];
+  LaunchCtx& cx = launch_ctx();
+  cudaStream_t& side = cx.q_side;
+  cudaEvent_t& fork_ev = cx.q_fork;
+  cudaEvent_t& join_ev = cx.q_join;
   if (!side) {
     TLRB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     TLRB_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));

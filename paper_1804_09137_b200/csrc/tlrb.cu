@@ -24,12 +24,14 @@
 //            left-lower TRSMs on contiguous columns.
 //   ws     : per-job compression workspace slots (M, E, Y, Q, Omega, B^T, V)
 #include "common.cuh"
+#include "comm.cuh"
 #include "../../include/tlrb200.h"
 #include <nccl.h>
 #include <cmath>
 #include <string>
 #include <chrono>
 #include <mutex>
+#include <thread>
 
 using namespace tlrb;
 
@@ -56,15 +58,24 @@ double factored_frac(int nb) {
   return v >= 0.0 ? v : (nb <= 512 ? 0.15 : 1.0);
 }
 
+// roofline denominators of tlrb_stats.t_roof_ms (tlrb_set_peaks)
+double g_peak_flops = 35.5e12, g_peak_bytes = 6449.7e9;
+
 struct Flops {
-  double f = 0, b = 0;
-  void add(double ff, double bb) { f += ff; b += bb; }
+  double f = 0, b = 0, troof = 0;   // troof: sum over ops of max(F / P64, B / BW), seconds
+  void add(double ff, double bb) {
+    f += ff;
+    b += bb;
+    troof += std::max(ff / g_peak_flops, bb / g_peak_bytes);
+  }
 };
 
 }  // namespace
 
 struct tlrb_handle {
   int device = 0;
+  int ctx = 0;                   // launch context slot (per-handle launcher caches)
+  std::recursive_mutex mu;       // calls on one handle take turns
   cudaStream_t stream = nullptr;
   // look-ahead stream: POTRF of the next diagonal tile overlaps the current
   // step's recompressions (factor_tlr)
@@ -85,11 +96,19 @@ struct tlrb_handle {
   double diam = 0.0;             // 2 * sphere radius; 0 => Euclidean
   std::vector<double> hxy;       // caller's (x, y) / (lon, lat), kept for tlrb_set_metric
   Pts pts() const { return Pts{dx, dy, dz, diam}; }
-  double* diag = nullptr;
+  double* diag = nullptr;         // the owned diagonal tiles, nb x nb each
+  std::vector<double*> dptr;     // per diagonal tile: its storage (nullptr: owned elsewhere)
+  double* lkk = nullptr;         // distributed: L_kk received from its owner (nb x nb)
+  // distributed: the panel tiles received at the current step (row and
+  // column broadcasts land in pbuf; their uptr / vptr point into it)
+  double* pbuf = nullptr;
+  size_t pbuf_cap = 0;           // doubles
+  std::vector<size_t> recv_tiles;
   // tile factors: rank-adaptive bump arena, reset at every factorisation;
   // tile t owns U (nb x tcap[t]) and V (nb x tcap[t]), or a dense nb x nb
   char* arena = nullptr;
   size_t arena_bytes = 0, arena_off = 0, arena_peak = 0;
+  size_t panel_peak = 0;           // largest received panel (distributed)
   std::vector<double*> uptr, vptr;
   std::vector<int> tcap;
   std::vector<int> rank;         // per lower tile
@@ -127,14 +146,21 @@ struct tlrb_handle {
   int retries = 0, max_sweeps = 0;
 
   // 2D block-cyclic distribution: tile (i, j) lives on rank
-  // (i mod P) * Q + (j mod Q); comm == nullptr -> single-GPU path
+  // (i mod P) * Q + (j mod Q); rank r sits in process row r / Q and process
+  // column r mod Q.  cw == nullptr -> single-GPU path.
   int drank = 0, dworld = 1, P = 1, Q = 1;
-  ncclComm_t comm = nullptr;
-  int* d_ibuf = nullptr;         // int all-reduce scratch (2 * ntile + 4)
+  std::unique_ptr<Comm> cw, crow, ccol;   // world, my process row (Q members), my process column (P members)
+  int* d_ibuf = nullptr;         // int all-reduce scratch (2 * ntile + 8)
   double* d_acc = nullptr;       // distributed solve accumulator (n)
-  bool dist() const { return comm != nullptr; }
+  bool dist() const { return cw != nullptr; }
+  int prow() const { return drank / Q; }
+  int pcol() const { return drank % Q; }
   int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
-  bool own(int i, int j) const { return !comm || owner(i, j) == drank; }
+  bool own(int i, int j) const { return !cw || owner(i, j) == drank; }
+  // group handle (tlrb_create with ngpus > 1, tlrb_create_group): one member
+  // handle per rank, each driven by its own host thread per call
+  std::vector<tlrb_handle*> members;
+  bool group() const { return !members.empty(); }
 
   size_t tid(int i, int j) const { return (size_t)i * (i - 1) / 2 + j; }
   bool dn(int i, int j) const { return dense[tid(i, j)] != 0; }
@@ -143,6 +169,7 @@ struct tlrb_handle {
   double* Vt(int i, int j) const { return vptr[tid(i, j)]; }
   void arena_reset() {
     arena_off = 0;
+    recv_tiles.clear();
     std::fill(uptr.begin(), uptr.end(), nullptr);
     std::fill(vptr.begin(), vptr.end(), nullptr);
     std::fill(tcap.begin(), tcap.end(), 0);
@@ -163,7 +190,9 @@ struct tlrb_handle {
     vptr[t] = dense_tile ? nullptr : arena_get((size_t)nb * c);
     tcap[t] = c;
   }
-  double* D(int i) const { return diag + (size_t)i * nb * nb; }
+  double* D(int i) const { return dptr[i]; }
+  // L_kk where the panel step needs it: owned, or received from its owner
+  double* Dk(int k) const { return dptr[k] ? dptr[k] : lkk; }
   void sync() {
     TLRB_CUDA(cudaStreamSynchronize(stream));
     // the arena is reset below: descriptors queued on the look-ahead stream
@@ -196,7 +225,8 @@ double now_ms() {
     if (r_ != ncclSuccess) throw CudaError(cudaErrorUnknown, ncclGetErrorString(r_), __FILE__, __LINE__); \
   } while (0)
 
-// all ranks learn every tile's rank / dense flag (owners contribute, others 0)
+// every rank learns every tile's rank / dense flag (owners contribute, others
+// 0): once per evaluation, after the factorisation (rank maps, statistics)
 void sync_ranks(tlrb_handle* h) {
   if (!h->dist()) return;
   const size_t nt = h->rank.size();
@@ -210,7 +240,7 @@ void sync_ranks(tlrb_handle* h) {
   if (nt) {
     TLRB_CUDA(cudaMemcpyAsync(h->d_ibuf, h->ar.put(buf, h->stream), 2 * nt * sizeof(int), cudaMemcpyDeviceToDevice,
                               h->stream));
-    TLRB_NCCL(ncclAllReduce(h->d_ibuf, h->d_ibuf, 2 * nt, ncclInt32, ncclSum, h->comm, h->stream));
+    h->cw->allreduce_sum(h->d_ibuf, 2 * nt, CType::I32, h->stream);
     TLRB_CUDA(cudaMemcpyAsync(buf.data(), h->d_ibuf, 2 * nt * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   }
   h->sync();
@@ -218,11 +248,6 @@ void sync_ranks(tlrb_handle* h) {
     h->rank[q] = buf[q];
     h->dense[q] = (char)buf[nt + q];
   }
-}
-
-void bcast(tlrb_handle* h, double* buf, size_t count, int root) {
-  if (!h->dist() || !count) return;
-  TLRB_NCCL(ncclBroadcast(buf, buf, count, ncclFloat64, root, h->comm, h->stream));
 }
 
 __global__ void axpy_kernel(double* y, const double* x, double a, int n) {
@@ -306,7 +331,14 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
   int info0 = 0;   // NPD flag of the POTRFs so far, read with the ranks (no extra sync)
   TLRB_CUDA(cudaMemcpyAsync(&info0, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
   h->sync();
-  if (info0) h->npd_seen = true;
+  if (info0) {   // a POTRF failed: the factorisation stops, the batch is not finished
+    h->npd_seen = true;
+    for (Job& J : jobs) {
+      J.out_rank = 0;
+      J.dense_out = false;
+    }
+    return;
+  }
   const double t_q1 = trace_on() ? now_ms() : 0;
   std::vector<int> kinds(nj);
   {
@@ -451,16 +483,14 @@ void compress_all(tlrb_handle* h, double acc) {
       h->work.add(4.0 * m * n * k, 8.0 * m * n + 8.0 * k * (m + n));
     }
   }
-  sync_ranks(h);
 }
 
 // ------------------------------------------------------------------ POTRF
+// L_kk on its owner (linalg.py:36-45); distributed handles then share it
+// down process column k mod Q, where the panel tiles (i, k) live (share_lkk)
 void potrf(tlrb_handle* h, int k, cudaStream_t s = nullptr) {
   if (!s) s = h->stream;
-  if (!h->own(k, k)) {   // L_kk arrives from its owner
-    bcast(h, h->D(k), (size_t)h->nb * h->nb, h->owner(k, k));
-    return;
-  }
+  if (!h->own(k, k)) return;
   const int n = h->sz[k];
   double* A = h->D(k);
   for (int r0 = 0; r0 < n; r0 += kPotrfBlock) {
@@ -477,51 +507,178 @@ void potrf(tlrb_handle* h, int k, cudaStream_t s = nullptr) {
   }
   const double nn = n;
   h->work.add(nn * nn * nn / 3.0, 16.0 * nn * nn);
-  bcast(h, h->D(k), (size_t)h->nb * h->nb, h->owner(k, k));
 }
 
-// panel tiles (i, k), i > k, from their owners to every rank
+void share_lkk(tlrb_handle* h, int k) {
+  if (!h->dist() || h->pcol() != k % h->Q) return;
+  double* buf = h->own(k, k) ? h->D(k) : h->lkk;
+  h->ccol->bcast(buf, (size_t)h->nb * h->nb, CType::F64, k % h->P, h->stream);
+}
+
+// One all-reduce per panel step (distributed): the NPD flag of POTRF(k) and
+// the ranks / dense flags of the panel tiles (i, k), i > k, which every rank
+// needs to size the received panel and build its updates.  Returns true on NPD.
+bool set_npd(tlrb_handle* h, const int* info) {
+  if (!info[0]) return false;
+  h->err_tile = info[1];
+  h->err_pivot = info[2];
+  char b[160];
+  snprintf(b, sizeof b, "covariance not positive definite at tile %d, pivot %d; consider adding a nugget",
+           info[1], info[2]);
+  h->msg = b;
+  return true;
+}
+
+// every rank's POTRF report [flag, tile, pivot] sits in its own slot of the
+// all-reduced buffer; the first failing tile wins (a failure poisons the
+// later diagonal tiles, which other ranks may also report)
+void first_failure(const int* slots, int world, int* info) {
+  info[0] = info[1] = info[2] = 0;
+  for (int r = 0; r < world; ++r)
+    if (slots[3 * r] && (!info[0] || slots[3 * r + 1] < info[1])) {
+      info[0] = 1;
+      info[1] = slots[3 * r + 1];
+      info[2] = slots[3 * r + 2];
+    }
+}
+
+// One all-reduce per panel step (distributed): the POTRF reports and the
+// ranks / dense flags of the panel tiles (i, k), i > k, which every rank
+// needs to size the received panel and build its updates.  Returns true on NPD.
+bool panel_meta(tlrb_handle* h, int k) {
+  const int t = h->t, W = h->dworld;
+  const int np = t - k - 1;
+  std::vector<int> buf(3 * (size_t)W + 2 * (size_t)np, 0);
+  int* meta = buf.data() + 3 * W;
+  for (int i = k + 1; i < t; ++i)
+    if (h->own(i, k)) {
+      meta[i - k - 1] = h->rank[h->tid(i, k)];
+      meta[np + i - k - 1] = h->dense[h->tid(i, k)];
+    }
+  int* d = h->d_ibuf;
+  TLRB_CUDA(cudaMemcpyAsync(d, h->ar.put(buf, h->stream), buf.size() * sizeof(int), cudaMemcpyDeviceToDevice,
+                            h->stream));
+  TLRB_CUDA(cudaMemcpyAsync(d + 3 * h->drank, h->d_info, 3 * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+  h->cw->allreduce_sum(d, buf.size(), CType::I32, h->stream);
+  TLRB_CUDA(cudaMemcpyAsync(buf.data(), d, buf.size() * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  h->sync();
+  meta = buf.data() + 3 * W;
+  for (int i = k + 1; i < t; ++i) {
+    h->rank[h->tid(i, k)] = meta[i - k - 1];
+    h->dense[h->tid(i, k)] = (char)meta[np + i - k - 1];
+  }
+  int info[3];
+  first_failure(buf.data(), W, info);
+  return set_npd(h, info);
+}
+
+// Panel broadcast of step k, one packed buffer per
+// broadcast.  Rank (p, q) needs L_ik for its tiles (i, j) — i mod P = p, the
+// panel owner is in its own process row — and L_jk — j mod Q = q:
+//   row step    in each process row p, member k mod Q sends its panel tiles
+//               (i, k), i mod P = p, packed, to the row;
+//   column step in each process column q, member p sends the tiles (j, k),
+//               j mod P = p, j mod Q = q (owned or just received), packed,
+//               to the column — one broadcast per p.
+// A packed tile is U (nb x c) then V (nb x c), c = its rank, or the whole
+// dense L_ik^T (nb x sz_i).  Receivers point the tile's factors into pbuf;
+// release_panel drops them after the step, so a rank only ever stores its own
+// tiles plus one panel.
+size_t packed_doubles(const tlrb_handle* h, int i, int k, bool dense_mode) {
+  if (dense_mode || h->dn(i, k)) return (size_t)h->nb * h->sz[i];
+  return 2 * (size_t)h->nb * h->rank[h->tid(i, k)];
+}
+
 void bcast_panel(tlrb_handle* h, int k, bool dense_mode) {
   if (!h->dist()) return;
-  TLRB_NCCL(ncclGroupStart());
-  for (int i = k + 1; i < h->t; ++i) {
-    const int root = h->owner(i, k);
-    if (dense_mode || h->dn(i, k)) {
-      h->ensure(h->tid(i, k), h->nb, true);
-      bcast(h, h->Ut(i, k), (size_t)h->nb * h->sz[i], root);
-    } else {
-      const size_t r = h->rank[h->tid(i, k)];
-      if (r) h->ensure(h->tid(i, k), (int)r);
-      bcast(h, h->Ut(i, k), (size_t)h->nb * r, root);
-      bcast(h, h->Vt(i, k), (size_t)h->nb * r, root);
+  const int t = h->t, nb = h->nb, P = h->P, Q = h->Q, myp = h->prow(), myq = h->pcol();
+  std::vector<int> rowt;   // row step tiles
+  size_t rowtot = 0;
+  for (int i = k + 1; i < t; ++i)
+    if (i % P == myp && packed_doubles(h, i, k, dense_mode)) {
+      rowt.push_back(i);
+      rowtot += packed_doubles(h, i, k, dense_mode);
     }
+  std::vector<std::vector<int>> colt(P);
+  std::vector<size_t> coltot(P, 0);
+  size_t coll = 0;
+  for (int j = k + 1; j < t; ++j)
+    if (j % Q == myq && packed_doubles(h, j, k, dense_mode)) {
+      colt[j % P].push_back(j);
+      coltot[j % P] += packed_doubles(h, j, k, dense_mode);
+    }
+  for (int p = 0; p < P; ++p) coll += coltot[p];
+  const size_t need = (Q > 1 ? rowtot : 0) + (P > 1 ? coll : 0);
+  if (need > h->pbuf_cap) {
+    h->sync();   // earlier steps' updates may still read the old panel
+    if (h->pbuf) TLRB_CUDA(cudaFree(h->pbuf));
+    h->pbuf_cap = std::max(need, h->pbuf_cap + h->pbuf_cap / 2);
+    TLRB_CUDA(cudaMalloc(&h->pbuf, h->pbuf_cap * sizeof(double)));
   }
-  TLRB_NCCL(ncclGroupEnd());
+  h->panel_peak = std::max(h->panel_peak, need * sizeof(double));
+  // pack (root) or point into (receiver) one broadcast's tiles
+  auto run = [&](const std::vector<int>& tiles, double* base, size_t tot, bool root, Comm& c, int croot) {
+    if (!tot) return;
+    std::vector<CopyProb> cp;
+    size_t o = 0;
+    for (int i : tiles) {
+      const size_t q = h->tid(i, k);
+      const bool dt = dense_mode || h->dn(i, k);
+      const int c1 = dt ? h->sz[i] : h->rank[q];
+      if (root) {
+        cp.push_back({h->uptr[q], nb, base + o, nb, nb, c1, 0, 1.0, 0, nullptr});
+        if (!dt) cp.push_back({h->vptr[q], nb, base + o + (size_t)nb * c1, nb, nb, c1, 0, 1.0, 0, nullptr});
+      } else {
+        h->uptr[q] = base + o;
+        h->vptr[q] = dt ? nullptr : base + o + (size_t)nb * c1;
+        h->tcap[q] = dt ? nb : c1;
+        h->recv_tiles.push_back(q);
+      }
+      o += dt ? (size_t)nb * c1 : 2 * (size_t)nb * c1;
+    }
+    if (root) launch_copy(cp, h->ar, h->stream);
+    c.bcast(base, tot, CType::F64, croot, h->stream);
+  };
+  double* base = h->pbuf;
+  if (Q > 1) {
+    run(rowt, base, rowtot, myq == k % Q, *h->crow, k % Q);
+    base += rowtot;
+  }
+  if (P > 1)
+    for (int p = 0; p < P; ++p) {
+      run(colt[p], base, coltot[p], myp == p, *h->ccol, p);
+      base += coltot[p];
+    }
+}
+
+// the received panel tiles of the step just finished are not kept
+void release_panel(tlrb_handle* h) {
+  for (size_t q : h->recv_tiles) {
+    h->uptr[q] = h->vptr[q] = nullptr;
+    h->tcap[q] = 0;
+  }
+  h->recv_tiles.clear();
 }
 
 bool check_npd(tlrb_handle* h) {
   int info[3];
-  const int* src = h->d_info;
   if (h->dist()) {   // the failing tile's owner reported it; everyone stops
-    int* tot = h->d_ibuf + 2 * h->rank.size();
-    TLRB_NCCL(ncclAllReduce(h->d_info, tot, 3, ncclInt32, ncclSum, h->comm, h->stream));
-    src = tot;
+    const int W = h->dworld;
+    std::vector<int> slots(3 * (size_t)W, 0);
+    int* d = h->d_ibuf;
+    TLRB_CUDA(cudaMemsetAsync(d, 0, slots.size() * sizeof(int), h->stream));
+    TLRB_CUDA(cudaMemcpyAsync(d + 3 * h->drank, h->d_info, 3 * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+    h->cw->allreduce_sum(d, slots.size(), CType::I32, h->stream);
+    TLRB_CUDA(cudaMemcpyAsync(slots.data(), d, slots.size() * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    h->sync();
+    first_failure(slots.data(), W, info);
+    return set_npd(h, info);
   }
-  TLRB_CUDA(cudaMemcpyAsync(info, src, sizeof info, cudaMemcpyDeviceToHost, h->stream));
+  TLRB_CUDA(cudaMemcpyAsync(info, h->d_info, sizeof info, cudaMemcpyDeviceToHost, h->stream));
   h->sync();
-  if (info[0] && !h->dist()) {   // a look-ahead POTRF may have been writing it: re-read settled
-    TLRB_CUDA(cudaMemcpy(info, src, sizeof info, cudaMemcpyDeviceToHost));
-  }
-  if (info[0]) {
-    h->err_tile = info[1];
-    h->err_pivot = info[2];
-    char b[160];
-    snprintf(b, sizeof b, "covariance not positive definite at tile %d, pivot %d; consider adding a nugget",
-             info[1], info[2]);
-    h->msg = b;
-    return true;
-  }
-  return false;
+  if (info[0])   // a look-ahead POTRF may have been writing it: re-read settled
+    TLRB_CUDA(cudaMemcpy(info, h->d_info, sizeof info, cudaMemcpyDeviceToHost));
+  return set_npd(h, info);
 }
 
 // ------------------------------------------------------ dense factorisation
@@ -529,9 +686,10 @@ bool factor_dense(tlrb_handle* h) {
   const int t = h->t, nb = h->nb;
   for (int k = 0; k < t; ++k) {
     potrf(h, k);
+    share_lkk(h, k);
     std::vector<TrsmProb> tp;
     for (int i = k + 1; i < t; ++i)
-      if (h->own(i, k)) tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
+      if (h->own(i, k)) tp.push_back({h->Dk(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
     launch_trsm(tp, false, h->ar, h->stream);
     bcast_panel(h, k, true);
     std::vector<GemmProb> gp;
@@ -554,6 +712,7 @@ bool factor_dense(tlrb_handle* h) {
     for (int i = k + 1; i < t; ++i)
       h->work.add(nk * nk * h->sz[i], 8.0 * (nk * nk / 2 + 2.0 * nk * h->sz[i]));
     launch_gemm(gp, h->ar, h->stream);
+    release_panel(h);
   }
   return !check_npd(h);
 }
@@ -571,24 +730,26 @@ bool factor_tlr(tlrb_handle* h, double acc) {
     const double tk0 = trace_on() ? now_ms() : 0;
     if (ahead == k) TLRB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_potrf, 0));
     else potrf(h, k);
+    share_lkk(h, k);
     // K4: V_ik <- L_kk^-1 V_ik (low-rank) / L_ik^T <- L_kk^-1 A_ik^T (dense, A13)
     std::vector<TrsmProb> tp;
     for (int i = k + 1; i < t; ++i) {
       const double nk = h->sz[k];
       if (!h->own(i, k)) continue;
       if (h->dn(i, k)) {
-        tp.push_back({h->D(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
+        tp.push_back({h->Dk(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
         h->work.add(nk * nk * h->sz[i], 8.0 * (nk * nk / 2 + 2.0 * nk * h->sz[i]));
         continue;
       }
       const int r = h->rank[h->tid(i, k)];
-      if (r) tp.push_back({h->D(k), nb, h->Vt(i, k), nb, h->sz[k], r});
+      if (r) tp.push_back({h->Dk(k), nb, h->Vt(i, k), nb, h->sz[k], r});
       if (r) h->work.add(nk * nk * r, 8.0 * (nk * nk / 2 + 2.0 * nk * r));
     }
     launch_trsm(tp, false, h->ar, h->stream);
     // single GPU: the NPD flag is read with the next rank readback (no sync
-    // here); a failed POTRF only lets this step's batch run on garbage
-    if (h->dist() ? check_npd(h) : (h->npd_seen && check_npd(h))) return false;
+    // here); a failed POTRF only lets this step's batch run on garbage.
+    // Distributed: one all-reduce carries the flag and the panel's ranks.
+    if (h->dist() ? panel_meta(h, k) : (h->npd_seen && check_npd(h))) return false;
     bcast_panel(h, k, false);
     // K5: D_j -= U_jk (V_jk^T V_jk) U_jk^T  (dense panel tile: D_j -= T_jk^T T_jk)
     {
@@ -685,6 +846,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_gemm(dt, h->ar, h->stream);
     }
     for (size_t c0 = 0; c0 < upd.size(); c0 += h->max_jobs) {
+      if (h->npd_seen) break;
       const size_t c1 = std::min(upd.size(), c0 + h->max_jobs);
       std::vector<Job> jobs;
       std::vector<GemmProb> gx, gy, gm, gm2;
@@ -919,8 +1081,10 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         h->dense[h->tid(i, j)] = J.dense_out;
       }
     }
-    sync_ranks(h);   // every rank learns the new ranks before the next panel broadcast
+    release_panel(h);
+    if (h->npd_seen) break;   // single GPU: a POTRF failed (read with a rank readback)
   }
+  sync_ranks(h);   // rank maps / statistics: every rank learns every tile's final rank
   return !check_npd(h);
 }
 
@@ -958,7 +1122,7 @@ void apply_factor(tlrb_handle* h, const double* dx, double* dy) {
       launch_gemm(g1, h->ar, h->stream);
       launch_gemm(g2, h->ar, h->stream);
     }
-    TLRB_NCCL(ncclAllReduce(dy, dy, h->n, ncclFloat64, ncclSum, h->comm, h->stream));
+    h->cw->allreduce_sum(dy, h->n, CType::F64, h->stream);
     return;
   }
   for (int i = 0; i < t; ++i) {   // the diagonal factors' upper parts are stale: clear them
@@ -1023,22 +1187,33 @@ void add_tile_times(tlrb_handle* h, int i, int j, const double* x, double* acc, 
   }
 }
 
+// Forward (linalg.py:166-177): for tile row j, the partial sums
+// acc_j = sum_{l<j} L_jl y_l live with the owners of (j, l), i.e. in process
+// row j mod P: reduced onto the owner of D_j (member j mod Q), which solves
+// y_j; y_j then goes down process column j mod Q, where the owners of (i, j),
+// i > j, add L_ij y_j into their accumulators.
+// Backward (linalg.py:180-197): the transpose — acc_j = sum_{i>j} L_ij^T x_i
+// lives in process column j mod Q (reduced onto member j mod P), and x_j goes
+// along process row j mod P to the owners of (j, l), l < j.
+// Each rank ends holding the solved tiles of its own diagonal tiles;
+// gather_solution assembles the full vector on every rank.
 void solve_dist(tlrb_handle* h, bool backward) {
-  const int t = h->t, nb = h->nb;
+  const int t = h->t, nb = h->nb, P = h->P, Q = h->Q, myp = h->prow(), myq = h->pcol();
   cudaStream_t s = h->stream;
   TLRB_CUDA(cudaMemsetAsync(h->d_acc, 0, h->n * sizeof(double), s));
   for (int q = 0; q < t; ++q) {
     const int j = backward ? t - 1 - q : q;
     double* zj = h->d_z + h->off[j];
     double* aj = h->d_acc + h->off[j];
-    const int root = h->owner(j, j);
-    TLRB_NCCL(ncclReduce(aj, aj, h->sz[j], ncclFloat64, ncclSum, root, h->comm, s));
+    if (!backward && myp == j % P) h->crow->reduce_sum(aj, h->sz[j], CType::F64, j % Q, s);
+    if (backward && myq == j % Q) h->ccol->reduce_sum(aj, h->sz[j], CType::F64, j % P, s);
     if (h->own(j, j)) {
       axpy_kernel<<<4, 256, 0, s>>>(zj, aj, -1.0, h->sz[j]);
       post_launch();
       launch_trsm({TrsmProb{h->D(j), nb, zj, h->sz[j], h->sz[j], 1}}, backward, h->ar, s);
     }
-    bcast(h, zj, h->sz[j], root);
+    if (!backward && myq == j % Q) h->ccol->bcast(zj, h->sz[j], CType::F64, j % P, s);
+    if (backward && myp == j % P) h->crow->bcast(zj, h->sz[j], CType::F64, j % Q, s);
     std::vector<GemmProb> g1, g2;
     if (!backward) {
       for (int i = j + 1; i < t; ++i)
@@ -1052,9 +1227,23 @@ void solve_dist(tlrb_handle* h, bool backward) {
   }
 }
 
+// every rank gets the whole solution: the owners of the diagonal tiles
+// contribute their solved tiles, one sum all-reduce of n doubles
+void gather_solution(tlrb_handle* h) {
+  if (!h->dist()) return;
+  cudaStream_t s = h->stream;
+  TLRB_CUDA(cudaMemsetAsync(h->d_acc, 0, h->n * sizeof(double), s));
+  for (int j = 0; j < h->t; ++j)
+    if (h->own(j, j))
+      TLRB_CUDA(cudaMemcpyAsync(h->d_acc + h->off[j], h->d_z + h->off[j], h->sz[j] * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+  h->cw->allreduce_sum(h->d_acc, h->n, CType::F64, s);
+  TLRB_CUDA(cudaMemcpyAsync(h->d_z, h->d_acc, h->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
 // ------------------------------------------------------------------ solves
 void forward_solve(tlrb_handle* h) {
-  if (h->dist()) { solve_dist(h, false); return; }
+  if (h->dist()) { solve_dist(h, false); gather_solution(h); return; }
   const int t = h->t, nb = h->nb;
   for (int j = 0; j < t; ++j) {
     double* yj = h->d_z + h->off[j];
@@ -1079,7 +1268,7 @@ void forward_solve(tlrb_handle* h) {
 }
 
 void backward_solve(tlrb_handle* h) {
-  if (h->dist()) { solve_dist(h, true); return; }
+  if (h->dist()) { solve_dist(h, true); gather_solution(h); return; }
   const int t = h->t, nb = h->nb;
   for (int i = t - 1; i >= 0; --i) {
     double* xi = h->d_z + h->off[i];
@@ -1183,14 +1372,14 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
   const auto t0 = std::chrono::steady_clock::now();
   TLRB_CUDA(cudaEventRecord(h->ev[5], s));
   TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double),
-                            z_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+                            z_on_device ? cudaMemcpyDefault : cudaMemcpyHostToDevice, s));
   rc = factorize(h, th1, th2, th3, nugget, acc);
   if (rc) return rc;
   forward_solve(h);
   launch_dot(h->d_z, (int)h->n, h->d_scal + 1, s);
   launch_sum_log(h->d_logdiag, (int)h->n, h->d_scal, s);
   if (h->dist())   // log-det: owners of the diagonal tiles hold the partial sums
-    TLRB_NCCL(ncclAllReduce(h->d_scal, h->d_scal, 1, ncclFloat64, ncclSum, h->comm, s));
+    h->cw->allreduce_sum(h->d_scal, 1, CType::F64, s);
   TLRB_CUDA(cudaEventRecord(h->ev[4], s));
   double sc[2];
   TLRB_CUDA(cudaMemcpyAsync(sc, h->d_scal, sizeof sc, cudaMemcpyDeviceToHost, s));
@@ -1199,7 +1388,7 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
   if (ll) *ll = -0.5 * (h->n * LOG_2PI + sc[0] + sc[1]);
   if (logdet) *logdet = sc[0];
   if (quad) *quad = sc[1];
-  if (st) {
+  {
     tlrb_stats S{};
     float a;
     TLRB_CUDA(cudaEventElapsedTime(&a, h->ev[0], h->ev[2])); S.ms_generate = a;
@@ -1232,18 +1421,25 @@ int loglik_impl(tlrb_handle* h, const double* z, bool z_on_device, double th1, d
     S.sketch_retries = h->retries;
     S.jacobi_max_sweeps = h->max_sweeps;
     S.kernel_launches = g_launches - l0;
-    *st = S;
+    S.t_roof_ms = h->work.troof * 1e3;
+    S.arena_peak_bytes = (int64_t)h->arena_peak;
+    S.panel_peak_bytes = (int64_t)h->panel_peak;
+    h->st = S;
+    if (st) *st = S;
   }
   return TLRB_OK;
 }
 
 template <class F>
 int guarded(tlrb_handle* h, F&& f) {
-  // launcher caches are per device and the DescArena / workspace per handle:
-  // calls that reach the same device from several host threads take turns
-  static std::recursive_mutex dev_mu[kMaxDevices];
+  // calls on one handle take turns (DescArena, workspace, streams); the
+  // launcher caches belong to the handle's launch context, so different
+  // handles — also several logical ranks on one device — run concurrently
   std::unique_lock<std::recursive_mutex> lk;
-  if (h && h->device >= 0 && h->device < kMaxDevices) lk = std::unique_lock<std::recursive_mutex>(dev_mu[h->device]);
+  if (h) {
+    lk = std::unique_lock<std::recursive_mutex>(h->mu);
+    set_thread_ctx(h->ctx);
+  }
   try {
     return f();
   } catch (const CudaError& e) {
@@ -1256,24 +1452,22 @@ int guarded(tlrb_handle* h, F&& f) {
   }
 }
 
-}  // namespace
-
-// =================================================================== C ABI
-extern "C" {
-
-tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus, int32_t max_rank,
-                         int32_t device, int32_t* err) {
-  if (err) *err = TLRB_OK;
-  // the compression kernels stage at most 2048 rows per column (QRCP / Jacobi
-  // register tiles of 64 doubles per lane): larger tiles are refused
-  if (!xy || n < 1 || nb < 1 || ngpus != 1 || std::min<int64_t>(nb, n) > kMaxTile) {
-    if (err) *err = TLRB_ERR_ARG;
-    return nullptr;
-  }
+// Allocate one (member) handle.  rank / P / Q: its place on the 2D
+// block-cyclic grid (0 / 1 / 1 single GPU) — only owned tiles get storage.
+// share / slot: handles created together on this device and this one's
+// index among them: the HBM budgets are split between them.
+tlrb_handle* create_one(const double* xy, int64_t n, int nb, int max_rank, int device, int rank, int P, int Q,
+                        int share, int slot, int32_t* err) {
   tlrb_handle* h = new tlrb_handle();
+  h->device = device;
   const int rc = guarded(h, [&]() -> int {
-    h->device = device;
     TLRB_CUDA(cudaSetDevice(device));
+    h->ctx = acquire_ctx();
+    set_thread_ctx(h->ctx);
+    h->drank = rank;
+    h->P = P;
+    h->Q = Q;
+    h->dworld = P * Q;
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->lane2, cudaStreamNonBlocking));
@@ -1299,13 +1493,24 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMemcpy(h->dy, ys.data(), n * sizeof(double), cudaMemcpyHostToDevice));
     const size_t nb2 = (size_t)h->nb * h->nb;
     const size_t ntile = (size_t)h->t * (h->t - 1) / 2;
-    TLRB_CUDA(cudaMalloc(&h->diag, std::max<size_t>(1, h->t * nb2) * sizeof(double)));
+    auto owns = [&](int i, int j) { return (i % P) * Q + (j % Q) == rank; };
+    size_t nd = 0, nlow = 0;
+    for (int i = 0; i < h->t; ++i) {
+      nd += owns(i, i);
+      for (int j = 0; j < i; ++j) nlow += owns(i, j);
+    }
+    TLRB_CUDA(cudaMalloc(&h->diag, std::max<size_t>(1, nd * nb2) * sizeof(double)));
+    h->dptr.assign(h->t, nullptr);
+    for (int i = 0, q = 0; i < h->t; ++i)
+      if (owns(i, i)) h->dptr[i] = h->diag + (size_t)(q++) * nb2;
+    if (P * Q > 1) TLRB_CUDA(cudaMalloc(&h->lkk, nb2 * sizeof(double)));
     h->uptr.assign(ntile, nullptr);
     h->vptr.assign(ntile, nullptr);
     h->tcap.assign(ntile, 0);
     h->rank.assign(ntile, 0);
     h->dense.assign(ntile, 0);
     TLRB_CUDA(cudaMalloc(&h->d_info, 4 * sizeof(int)));
+    TLRB_CUDA(cudaMemset(h->d_info, 0, 4 * sizeof(int)));   // no POTRF failure yet
     TLRB_CUDA(cudaMalloc(&h->d_logdiag, n * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_scal, 4 * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_z, n * sizeof(double)));
@@ -1317,11 +1522,14 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMemGetInfo(&freeb, &totb));
     // capped at 56 GB for tile grids up to 128 x 128 (fewer, larger job
     // batches: C3 16.3 s vs 17.2 s at 24 GB) and at 24 GB beyond, where the
-    // rank-adaptive factor arena needs the rest of HBM (C4, C5); TLRB_WS_GB overrides
+    // rank-adaptive factor arena needs the rest of HBM (C4, C5); TLRB_WS_GB
+    // overrides.  Handles created together on one device split the budget.
     const size_t cap_gb = getenv("TLRB_WS_GB") ? (size_t)atoll(getenv("TLRB_WS_GB")) : (h->t <= 128 ? 56 : 24);
-    size_t budget = std::min<size_t>(freeb / 3, cap_gb << 30);
+    const int left = std::max(1, share - slot);   // handles of this group still to size on the device
+    size_t budget = std::min<size_t>(freeb / 3 / left, (cap_gb << 30) / std::max(1, share));
+    const size_t owned_jobs = std::max<size_t>(nlow, 1);
     int jobs = (int)std::max<size_t>(1, budget / (h->slot_doubles * 8));
-    jobs = (int)std::min<size_t>(jobs, std::max<size_t>(ntile, 1));
+    jobs = (int)std::min<size_t>(jobs, owned_jobs);
     h->max_jobs = std::min(jobs, 8192);
     h->ws_bytes = std::max((size_t)h->max_jobs * h->slot_doubles * 8, nb2 * 8 * 4);
     TLRB_CUDA(cudaMalloc(&h->ws, h->ws_bytes));
@@ -1333,10 +1541,13 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
     TLRB_CUDA(cudaMalloc(&h->d_sweeps, (size_t)h->max_jobs * sizeof(int)));
     TLRB_CUDA(cudaMalloc(&h->d_perm, (size_t)h->max_jobs * h->nb * sizeof(int)));
     {
+      // the factor arena holds this rank's own tiles only (received panel
+      // tiles live in pbuf): at most all of them dense, twice (a tile whose
+      // rank grows gets a fresh slot), within 85% of what is left
       size_t fb = 0, tb = 0;
       TLRB_CUDA(cudaMemGetInfo(&fb, &tb));
-      const size_t full = std::max<size_t>(1, ntile) * 2 * nb2 * sizeof(double) + (1 << 20);
-      const size_t avail = (size_t)(0.85 * (double)fb);
+      const size_t full = std::max<size_t>(1, nlow) * 2 * nb2 * sizeof(double) + (1 << 20);
+      const size_t avail = (size_t)(0.85 * (double)fb / left);
       h->arena_bytes = std::min(full, avail);
       TLRB_CUDA(cudaMalloc(&h->arena, h->arena_bytes));
     }
@@ -1351,6 +1562,300 @@ tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus,
   return h;
 }
 
+// distributed scratch, once the communicators are attached
+int attach_dist(tlrb_handle* h) {
+  return guarded(h, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(h->device));
+    TLRB_CUDA(cudaMalloc(&h->d_ibuf, (2 * h->rank.size() + 3 * (size_t)h->dworld + 8) * sizeof(int)));
+    TLRB_CUDA(cudaMalloc(&h->d_acc, h->n * sizeof(double)));
+    return TLRB_OK;
+  });
+}
+
+// Run fn(member, index) for every member of a group handle, one host thread
+// each (the members' collectives rendezvous with one another).  A CUDA
+// failure on one member aborts the loopback communicators so that the others
+// leave their collectives instead of waiting forever.
+template <class F>
+int run_members(tlrb_handle* g, F&& fn) {
+  const int W = (int)g->members.size();
+  std::vector<int> rc(W, TLRB_OK);
+  std::vector<std::thread> th;
+  for (int r = 0; r < W; ++r)
+    th.emplace_back([&, r] {
+      tlrb_handle* m = g->members[r];
+      rc[r] = guarded(m, [&]() -> int {
+        TLRB_CUDA(cudaSetDevice(m->device));
+        return fn(m, r);
+      });
+      if (rc[r] == TLRB_ERR_CUDA)
+        for (tlrb_handle* o : g->members)
+          for (Comm* c : {o->cw.get(), o->crow.get(), o->ccol.get()})
+            if (c && !strcmp(c->kind(), "loopback")) c->abort();
+    });
+  for (auto& x : th) x.join();
+  int out = TLRB_OK;
+  for (int r = 0; r < W && out == TLRB_OK; ++r)
+    if (rc[r] != TLRB_OK) {
+      out = rc[r];
+      g->msg = g->members[r]->msg;
+      g->err_tile = g->members[r]->err_tile;
+      g->err_pivot = g->members[r]->err_pivot;
+    }
+  // a genuine failure (not an NPD, which every member reports) wins
+  for (int r = 0; r < W; ++r)
+    if (rc[r] == TLRB_ERR_CUDA) {
+      out = rc[r];
+      g->msg = g->members[r]->msg;
+      break;
+    }
+  return out;
+}
+
+void grid_shape(int world, int& P, int& Q) {
+  // P x Q with P <= Q, as square as possible (1x1, 1x2, 2x2, 2x4, ...)
+  P = 1;
+  for (int p = 1; p * p <= world; ++p)
+    if (world % p == 0) P = p;
+  Q = world / P;
+}
+
+tlrb_handle* create_group(const double* xy, int64_t n, int32_t nb, int32_t max_rank, const int32_t* devices,
+                          int32_t world, int32_t P, int32_t Q, int32_t backend, int32_t* err) {
+  if (err) *err = TLRB_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+  cudaGetLastError();
+  bool distinct = true;
+  for (int r = 0; r < world; ++r) {
+    if (devices[r] < 0 || devices[r] >= ndev) {
+      if (err) *err = TLRB_ERR_ARG;
+      return nullptr;
+    }
+    for (int q = 0; q < r; ++q) distinct &= devices[q] != devices[r];
+  }
+  if (backend == TLRB_BACKEND_AUTO) backend = distinct ? TLRB_BACKEND_NCCL : TLRB_BACKEND_LOOPBACK;
+  if (backend == TLRB_BACKEND_NCCL && !distinct) {   // NCCL takes one rank per device
+    if (err) *err = TLRB_ERR_ARG;
+    return nullptr;
+  }
+  tlrb_handle* g = new tlrb_handle();
+  g->device = devices[0];
+  g->dworld = world;
+  g->P = P;
+  g->Q = Q;
+  g->n = n;
+  g->nb = (int)std::min<int64_t>(nb, n);
+  g->t = (int)((n + g->nb - 1) / g->nb);
+  std::vector<int> share(world), slot(world);
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q)
+      if (devices[q] == devices[r]) {
+        ++share[r];
+        if (q < r) ++slot[r];
+      }
+  for (int r = 0; r < world; ++r) {
+    tlrb_handle* m = create_one(xy, n, nb, max_rank, devices[r], r, P, Q, share[r], slot[r], err);
+    if (!m) {
+      tlrb_destroy(g);
+      return nullptr;
+    }
+    g->members.push_back(m);
+  }
+  int rc = TLRB_OK;
+  try {
+    if (backend == TLRB_BACKEND_LOOPBACK) {
+      auto wg = make_local_group(world);
+      std::vector<std::shared_ptr<LocalGroup>> rows, cols;
+      for (int p = 0; p < P; ++p) rows.push_back(make_local_group(Q));
+      for (int q = 0; q < Q; ++q) cols.push_back(make_local_group(P));
+      for (int r = 0; r < world; ++r) {
+        tlrb_handle* m = g->members[r];
+        TLRB_CUDA(cudaSetDevice(m->device));
+        m->cw = make_local_comm(wg, r, m->device);
+        m->crow = make_local_comm(rows[r / Q], r % Q, m->device);
+        m->ccol = make_local_comm(cols[r % Q], r / Q, m->device);
+      }
+    } else {
+      std::vector<ncclComm_t> comms(world);
+      TLRB_NCCL(ncclCommInitAll(comms.data(), world, devices));
+      for (int r = 0; r < world; ++r) g->members[r]->cw = make_nccl_comm(comms[r]);
+      // row / column communicators: ncclCommSplit is collective over the
+      // world members, one host thread each
+      rc = run_members(g, [&](tlrb_handle* m, int r) -> int {
+        m->crow = split_nccl_comm(*m->cw, r / Q, r % Q);
+        m->ccol = split_nccl_comm(*m->cw, Q + r % Q, r / Q);
+        return TLRB_OK;
+      });
+    }
+  } catch (const CudaError& e) {
+    g->msg = e.msg;
+    rc = TLRB_ERR_CUDA;
+  }
+  for (int r = 0; r < world && rc == TLRB_OK; ++r) rc = attach_dist(g->members[r]);
+  if (rc != TLRB_OK) {
+    if (err) *err = rc;
+    fprintf(stderr, "tlrb_create_group: %s\n", g->msg.c_str());
+    tlrb_destroy(g);
+    return nullptr;
+  }
+  return g;
+}
+
+// the group's statistics: member 0's, with the slowest member's device time
+// and the largest per-member memory high-water marks
+void group_stats(tlrb_handle* g, std::vector<tlrb_stats>& ms, tlrb_stats* st) {
+  if (!st) return;
+  tlrb_stats S = ms[0];
+  for (const tlrb_stats& m : ms) {
+    S.ms_device = std::max(S.ms_device, m.ms_device);
+    S.ms_total = std::max(S.ms_total, m.ms_total);
+    S.arena_peak_bytes = std::max(S.arena_peak_bytes, m.arena_peak_bytes);
+    S.panel_peak_bytes = std::max(S.panel_peak_bytes, m.panel_peak_bytes);
+  }
+  S.kernel_launches = 0;
+  for (const tlrb_stats& m : ms) S.kernel_launches += m.kernel_launches;
+  *st = S;
+}
+
+int loglik_any(tlrb_handle* h, const double* z, bool on_dev, double th1, double th2, double th3, double nugget,
+               double acc, double* ll, double* logdet, double* quad, tlrb_stats* st) {
+  if (!h->group())
+    return guarded(h, [&] { return loglik_impl(h, z, on_dev, th1, th2, th3, nugget, acc, ll, logdet, quad, st); });
+  std::vector<tlrb_stats> ms(h->members.size());
+  std::vector<double> out(3 * h->members.size());
+  const int rc = run_members(h, [&](tlrb_handle* m, int r) {
+    return loglik_impl(m, z, on_dev, th1, th2, th3, nugget, acc, &out[3 * r], &out[3 * r + 1], &out[3 * r + 2],
+                       &ms[r]);
+  });
+  if (rc) return rc;
+  if (ll) *ll = out[0];
+  if (logdet) *logdet = out[1];
+  if (quad) *quad = out[2];
+  group_stats(h, ms, st);
+  return TLRB_OK;
+}
+
+int factorize_one(tlrb_handle* h, double th1, double th2, double th3, double nugget, double acc) {
+  TLRB_CUDA(cudaSetDevice(h->device));
+  const int r = factorize(h, th1, th2, th3, nugget, acc);
+  h->sync();
+  return r;
+}
+
+int apply_factor_one(tlrb_handle* h, const double* x, double* y) {
+  if (!h->factor_mode) {
+    h->msg = "no factor available";
+    return TLRB_ERR_ARG;
+  }
+  TLRB_CUDA(cudaSetDevice(h->device));
+  if (!h->d_y) TLRB_CUDA(cudaMalloc(&h->d_y, h->n * sizeof(double)));
+  TLRB_CUDA(cudaMemcpyAsync(h->d_z, x, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  apply_factor(h, h->d_z, h->d_y);
+  if (y) TLRB_CUDA(cudaMemcpyAsync(y, h->d_y, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  h->sync();
+  return TLRB_OK;
+}
+
+int solve_one(tlrb_handle* h, const double* rhs, double* x) {
+  if (!h->factor_mode) {
+    h->msg = "no factor available";
+    return TLRB_ERR_ARG;
+  }
+  TLRB_CUDA(cudaSetDevice(h->device));
+  TLRB_CUDA(cudaMemcpyAsync(h->d_z, rhs, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  forward_solve(h);
+  backward_solve(h);
+  if (x) TLRB_CUDA(cudaMemcpyAsync(x, h->d_z, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  h->sync();
+  return TLRB_OK;
+}
+
+int predict_one(tlrb_handle* h, const double* z, const double* xy_unknown, int64_t m, double th1, double th2,
+                double th3, double nugget, double acc, double* pred) {
+  TLRB_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  if (m > h->ucap) {
+    if (h->d_ux) { cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_uz); cudaFree(h->d_pred); cudaFree(h->d_partial); }
+    h->ucap = m;
+    const int64_t nchunk = (h->n + 2047) / 2048;
+    TLRB_CUDA(cudaMalloc(&h->d_ux, m * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_uy, m * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_uz, m * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_pred, m * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_partial, m * nchunk * sizeof(double)));
+  }
+  std::vector<double> ux, uy, uz;
+  if (kernel_view(xy_unknown, m, 0.5 * h->diam, ux, uy, uz)) return TLRB_ERR_ARG;
+  TLRB_CUDA(cudaMemcpyAsync(h->d_ux, ux.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+  TLRB_CUDA(cudaMemcpyAsync(h->d_uy, uy.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (h->diam > 0.0)
+    TLRB_CUDA(cudaMemcpyAsync(h->d_uz, uz.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+  TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double), cudaMemcpyHostToDevice, s));
+  int r = factorize(h, th1, th2, th3, nugget, acc);
+  if (r) return r;
+  forward_solve(h);
+  backward_solve(h);
+  if (pred) {   // group handles: one member forms the cross-covariance product
+    launch_cross_gemv(h->pts(), h->d_z, h->n, Pts{h->d_ux, h->d_uy, h->d_uz, h->diam}, m, h->mp,
+                      h->d_partial, h->d_pred, s);
+    TLRB_CUDA(cudaMemcpyAsync(pred, h->d_pred, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  h->sync();
+  return TLRB_OK;
+}
+
+int set_metric_one(tlrb_handle* h, const std::vector<double>& a1, const std::vector<double>& a2,
+                   const std::vector<double>& a3, double sphere_radius) {
+  TLRB_CUDA(cudaSetDevice(h->device));
+  TLRB_CUDA(cudaStreamSynchronize(h->stream));
+  TLRB_CUDA(cudaMemcpy(h->dx, a1.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
+  TLRB_CUDA(cudaMemcpy(h->dy, a2.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
+  if (!a3.empty()) {
+    if (!h->dz) TLRB_CUDA(cudaMalloc(&h->dz, h->n * sizeof(double)));
+    TLRB_CUDA(cudaMemcpy(h->dz, a3.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  h->diam = 2.0 * sphere_radius;
+  return TLRB_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+tlrb_handle* tlrb_create(const double* xy, int64_t n, int32_t nb, int32_t ngpus, int32_t max_rank,
+                         int32_t device, int32_t* err) {
+  if (err) *err = TLRB_OK;
+  // the compression kernels stage at most 2048 rows per column (QRCP / Jacobi
+  // register tiles of 64 doubles per lane): larger tiles are refused
+  if (!xy || n < 1 || nb < 1 || ngpus < 1 || ngpus > kMaxDevices || device < 0 ||
+      std::min<int64_t>(nb, n) > kMaxTile) {
+    if (err) *err = TLRB_ERR_ARG;
+    return nullptr;
+  }
+  if (ngpus == 1) return create_one(xy, n, nb, max_rank, device, 0, 1, 1, 1, 0, err);
+  // one process driving devices device .. device + ngpus - 1 (NCCL over
+  // NVLink between them, one host thread per device inside each call)
+  std::vector<int32_t> devs(ngpus);
+  for (int r = 0; r < ngpus; ++r) devs[r] = device + r;
+  int P = 1, Q = 1;
+  grid_shape(ngpus, P, Q);
+  return create_group(xy, n, nb, max_rank, devs.data(), ngpus, P, Q, TLRB_BACKEND_AUTO, err);
+}
+
+tlrb_handle* tlrb_create_group(const double* xy, int64_t n, int32_t nb, int32_t max_rank,
+                               const int32_t* devices, int32_t world, int32_t P, int32_t Q, int32_t backend,
+                               int32_t* err) {
+  if (err) *err = TLRB_OK;
+  if (!xy || !devices || n < 1 || nb < 1 || world < 1 || world > 64 || P < 1 || Q < 1 || P * Q != world ||
+      backend < TLRB_BACKEND_AUTO || backend > TLRB_BACKEND_LOOPBACK || std::min<int64_t>(nb, n) > kMaxTile) {
+    if (err) *err = TLRB_ERR_ARG;
+    return nullptr;
+  }
+  return create_group(xy, n, nb, max_rank, devices, world, P, Q, backend, err);
+}
+
 int32_t tlrb_nccl_unique_id(char* out, int32_t len) {
   if (!out || len < (int32_t)sizeof(ncclUniqueId)) return TLRB_ERR_ARG;
   ncclUniqueId id;
@@ -1363,24 +1868,24 @@ tlrb_handle* tlrb_create_dist(const double* xy, int64_t n, int32_t nb, int32_t m
                               int32_t rank, int32_t world, int32_t P, int32_t Q, const char* nccl_id,
                               int32_t* err) {
   if (err) *err = TLRB_OK;
-  if (!nccl_id || world < 1 || rank < 0 || rank >= world || P < 1 || Q < 1 || P * Q != world) {
+  if (!xy || !nccl_id || n < 1 || nb < 1 || world < 1 || rank < 0 || rank >= world || P < 1 || Q < 1 ||
+      P * Q != world || std::min<int64_t>(nb, n) > kMaxTile) {
     if (err) *err = TLRB_ERR_ARG;
     return nullptr;
   }
-  tlrb_handle* h = tlrb_create(xy, n, nb, 1, max_rank, device, err);
+  tlrb_handle* h = create_one(xy, n, nb, max_rank, device, rank, P, Q, 1, 0, err);
   if (!h) return nullptr;
-  const int rc = guarded(h, [&]() -> int {
+  int rc = guarded(h, [&]() -> int {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof id);
-    h->drank = rank;
-    h->dworld = world;
-    h->P = P;
-    h->Q = Q;
-    TLRB_NCCL(ncclCommInitRank(&h->comm, world, id, rank));
-    TLRB_CUDA(cudaMalloc(&h->d_ibuf, (2 * h->rank.size() + 8) * sizeof(int)));
-    TLRB_CUDA(cudaMalloc(&h->d_acc, h->n * sizeof(double)));
+    ncclComm_t c = nullptr;
+    TLRB_NCCL(ncclCommInitRank(&c, world, id, rank));
+    h->cw = make_nccl_comm(c);
+    h->crow = split_nccl_comm(*h->cw, rank / Q, rank % Q);
+    h->ccol = split_nccl_comm(*h->cw, Q + rank % Q, rank / Q);
     return TLRB_OK;
   });
+  if (rc == TLRB_OK) rc = attach_dist(h);
   if (rc != TLRB_OK) {
     if (err) *err = rc;
     fprintf(stderr, "tlrb_create_dist: %s\n", h->msg.c_str());
@@ -1392,14 +1897,16 @@ tlrb_handle* tlrb_create_dist(const double* xy, int64_t n, int32_t nb, int32_t m
 
 void tlrb_destroy(tlrb_handle* h) {
   if (!h) return;
+  for (tlrb_handle* m : h->members) tlrb_destroy(m);
+  h->members.clear();
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  if (h->comm) ncclCommDestroy(h->comm);
-  if (h->d_ibuf) cudaFree(h->d_ibuf);
-  if (h->d_acc) cudaFree(h->d_acc);
+  h->cw.reset();
+  h->crow.reset();
+  h->ccol.reset();
   void* ptrs[] = {h->dx, h->dy, h->dz, h->d_uz, h->diag, h->arena, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
                   h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_y, h->d_ux, h->d_uy,
-                  h->d_pred, h->d_partial};
+                  h->d_pred, h->d_partial, h->d_ibuf, h->d_acc, h->lkk, h->pbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->ar.release();
@@ -1412,66 +1919,53 @@ void tlrb_destroy(tlrb_handle* h) {
   if (h->ev_f) cudaEventDestroy(h->ev_f);
   if (h->ev_syrk) cudaEventDestroy(h->ev_syrk);
   if (h->ev_potrf) cudaEventDestroy(h->ev_potrf);
+  if (h->ctx) release_ctx(h->ctx);
   delete h;
+}
+
+int32_t tlrb_group_size(tlrb_handle* h) { return !h ? 0 : h->group() ? (int32_t)h->members.size() : 1; }
+
+int32_t tlrb_member_stats(tlrb_handle* h, int32_t member, tlrb_stats* st) {
+  if (!h || !st || member < 0 || member >= tlrb_group_size(h)) return TLRB_ERR_ARG;
+  tlrb_handle* m = h->group() ? h->members[member] : h;
+  *st = m->st;
+  return TLRB_OK;
 }
 
 int32_t tlrb_loglik(tlrb_handle* h, const double* z, double th1, double th2, double th3, double nugget,
                     double acc, double* ll, double* logdet, double* quad, tlrb_stats* st) {
   if (!h || !z) return TLRB_ERR_ARG;
-  return guarded(h, [&] { return loglik_impl(h, z, false, th1, th2, th3, nugget, acc, ll, logdet, quad, st); });
+  return loglik_any(h, z, false, th1, th2, th3, nugget, acc, ll, logdet, quad, st);
 }
 
 int32_t tlrb_loglik_device(tlrb_handle* h, const double* d_z, double th1, double th2, double th3,
                            double nugget, double acc, double* ll, double* logdet, double* quad,
                            tlrb_stats* st) {
   if (!h || !d_z) return TLRB_ERR_ARG;
-  return guarded(h, [&] { return loglik_impl(h, d_z, true, th1, th2, th3, nugget, acc, ll, logdet, quad, st); });
+  return loglik_any(h, d_z, true, th1, th2, th3, nugget, acc, ll, logdet, quad, st);
 }
 
 int32_t tlrb_factorize(tlrb_handle* h, double th1, double th2, double th3, double nugget, double acc) {
   if (!h) return TLRB_ERR_ARG;
   const int rc = validate(th1, th2, th3, nugget, acc);
   if (rc) return rc;
-  return guarded(h, [&]() -> int {
-    TLRB_CUDA(cudaSetDevice(h->device));
-    const int r = factorize(h, th1, th2, th3, nugget, acc);
-    h->sync();
-    return r;
-  });
+  if (h->group())
+    return run_members(h, [&](tlrb_handle* m, int) { return factorize_one(m, th1, th2, th3, nugget, acc); });
+  return guarded(h, [&] { return factorize_one(h, th1, th2, th3, nugget, acc); });
 }
 
 int32_t tlrb_apply_factor(tlrb_handle* h, const double* x, double* y) {
   if (!h || !x || !y) return TLRB_ERR_ARG;
-  if (!h->factor_mode) {
-    h->msg = "no factor available";
-    return TLRB_ERR_ARG;
-  }
-  return guarded(h, [&]() -> int {
-    TLRB_CUDA(cudaSetDevice(h->device));
-    if (!h->d_y) TLRB_CUDA(cudaMalloc(&h->d_y, h->n * sizeof(double)));
-    TLRB_CUDA(cudaMemcpyAsync(h->d_z, x, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    apply_factor(h, h->d_z, h->d_y);
-    TLRB_CUDA(cudaMemcpyAsync(y, h->d_y, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    h->sync();
-    return TLRB_OK;
-  });
+  if (h->group())
+    return run_members(h, [&](tlrb_handle* m, int r) { return apply_factor_one(m, x, r ? nullptr : y); });
+  return guarded(h, [&] { return apply_factor_one(h, x, y); });
 }
 
 int32_t tlrb_solve(tlrb_handle* h, const double* rhs, double* x) {
   if (!h || !rhs || !x) return TLRB_ERR_ARG;
-  if (!h->factor_mode) {
-    h->msg = "no factor available";
-    return TLRB_ERR_ARG;
-  }
-  return guarded(h, [&]() -> int {
-    TLRB_CUDA(cudaSetDevice(h->device));
-    TLRB_CUDA(cudaMemcpyAsync(h->d_z, rhs, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    forward_solve(h);
-    backward_solve(h);
-    TLRB_CUDA(cudaMemcpyAsync(x, h->d_z, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    h->sync();
-    return TLRB_OK;
-  });
+  if (h->group())
+    return run_members(h, [&](tlrb_handle* m, int r) { return solve_one(m, rhs, r ? nullptr : x); });
+  return guarded(h, [&] { return solve_one(h, rhs, x); });
 }
 
 int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown, int64_t m, double th1,
@@ -1479,40 +1973,16 @@ int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown, 
   if (!h || !z || !xy_unknown || !pred || m < 1) return TLRB_ERR_ARG;
   int rc = validate(th1, th2, th3, nugget, acc);
   if (rc) return rc;
-  return guarded(h, [&]() -> int {
-    TLRB_CUDA(cudaSetDevice(h->device));
-    cudaStream_t s = h->stream;
-    if (m > h->ucap) {
-      if (h->d_ux) { cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_uz); cudaFree(h->d_pred); cudaFree(h->d_partial); }
-      h->ucap = m;
-      const int64_t nchunk = (h->n + 2047) / 2048;
-      TLRB_CUDA(cudaMalloc(&h->d_ux, m * sizeof(double)));
-      TLRB_CUDA(cudaMalloc(&h->d_uy, m * sizeof(double)));
-      TLRB_CUDA(cudaMalloc(&h->d_uz, m * sizeof(double)));
-      TLRB_CUDA(cudaMalloc(&h->d_pred, m * sizeof(double)));
-      TLRB_CUDA(cudaMalloc(&h->d_partial, m * nchunk * sizeof(double)));
-    }
-    std::vector<double> ux, uy, uz;
-    if (kernel_view(xy_unknown, m, 0.5 * h->diam, ux, uy, uz)) return TLRB_ERR_ARG;
-    TLRB_CUDA(cudaMemcpyAsync(h->d_ux, ux.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
-    TLRB_CUDA(cudaMemcpyAsync(h->d_uy, uy.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
-    if (h->diam > 0.0)
-      TLRB_CUDA(cudaMemcpyAsync(h->d_uz, uz.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
-    TLRB_CUDA(cudaMemcpyAsync(h->d_z, z, h->n * sizeof(double), cudaMemcpyHostToDevice, s));
-    int r = factorize(h, th1, th2, th3, nugget, acc);
-    if (r) return r;
-    forward_solve(h);
-    backward_solve(h);
-    launch_cross_gemv(h->pts(), h->d_z, h->n, Pts{h->d_ux, h->d_uy, h->d_uz, h->diam}, m, h->mp,
-                      h->d_partial, h->d_pred, s);
-    TLRB_CUDA(cudaMemcpyAsync(pred, h->d_pred, m * sizeof(double), cudaMemcpyDeviceToHost, s));
-    h->sync();
-    return TLRB_OK;
-  });
+  if (h->group())
+    return run_members(h, [&](tlrb_handle* mm, int r) {
+      return predict_one(mm, z, xy_unknown, m, th1, th2, th3, nugget, acc, r ? nullptr : pred);
+    });
+  return guarded(h, [&] { return predict_one(h, z, xy_unknown, m, th1, th2, th3, nugget, acc, pred); });
 }
 
 int32_t tlrb_rank_map(tlrb_handle* h, int32_t* ranks, int32_t cap, int32_t* t_out) {
   if (!h) return TLRB_ERR_ARG;
+  if (h->group()) return tlrb_rank_map(h->members[0], ranks, cap, t_out);
   if (t_out) *t_out = h->t;
   if (!ranks) return TLRB_OK;
   if (cap < h->t * h->t) return TLRB_ERR_ARG;
@@ -1595,19 +2065,13 @@ int32_t tlrb_matern_block_metric(const double* rows_xy, int64_t m, const double*
 int32_t tlrb_set_metric(tlrb_handle* h, double sphere_radius) {
   if (!h) return TLRB_ERR_ARG;
   std::vector<double> a1, a2, a3;
-  if (kernel_view(h->hxy.data(), h->n, sphere_radius, a1, a2, a3)) return TLRB_ERR_ARG;
-  return guarded(h, [&]() -> int {
-    TLRB_CUDA(cudaSetDevice(h->device));
-    TLRB_CUDA(cudaStreamSynchronize(h->stream));
-    TLRB_CUDA(cudaMemcpy(h->dx, a1.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
-    TLRB_CUDA(cudaMemcpy(h->dy, a2.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
-    if (!a3.empty()) {
-      if (!h->dz) TLRB_CUDA(cudaMalloc(&h->dz, h->n * sizeof(double)));
-      TLRB_CUDA(cudaMemcpy(h->dz, a3.data(), h->n * sizeof(double), cudaMemcpyHostToDevice));
-    }
+  const std::vector<double>& xy = h->group() ? h->members[0]->hxy : h->hxy;
+  if (kernel_view(xy.data(), h->n, sphere_radius, a1, a2, a3)) return TLRB_ERR_ARG;
+  if (h->group()) {
     h->diam = 2.0 * sphere_radius;
-    return TLRB_OK;
-  });
+    return run_members(h, [&](tlrb_handle* m, int) { return set_metric_one(m, a1, a2, a3, sphere_radius); });
+  }
+  return guarded(h, [&] { return set_metric_one(h, a1, a2, a3, sphere_radius); });
 }
 
 int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc, int32_t* rank, double* u,
@@ -1658,6 +2122,19 @@ int32_t tlrb_profile_enable(int32_t on) {
 
 int32_t tlrb_profile_mask(uint32_t mask) {
   g_prof.mask = mask;
+  return TLRB_OK;
+}
+
+int32_t tlrb_set_peaks(double fp64_tflops, double hbm_gbs) {
+  if (!(fp64_tflops > 0) || !(hbm_gbs > 0)) return TLRB_ERR_ARG;
+  g_peak_flops = fp64_tflops * 1e12;
+  g_peak_bytes = hbm_gbs * 1e9;
+  return TLRB_OK;
+}
+
+int32_t tlrb_profile_busy(int32_t cls, double* busy_ms) {
+  if (cls >= K_NCLASS || !busy_ms) return TLRB_ERR_ARG;
+  *busy_ms = g_prof.busy_ms(cls);
   return TLRB_OK;
 }
 

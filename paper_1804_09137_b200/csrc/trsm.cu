@@ -139,12 +139,10 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
   }
   ProfScope ps(K_TRSM, s, fl, by);
   if (trans) {
-    TLRB_CUDA(cudaFuncSetAttribute(trsm_vbatch_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    allow_smem(trsm_vbatch_kernel<true>, smem);
     trsm_vbatch_kernel<true><<<tot, threads, smem, s>>>(dp, ds, (int)keep.size(), W);
   } else {
-    TLRB_CUDA(cudaFuncSetAttribute(trsm_vbatch_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    allow_smem(trsm_vbatch_kernel<false>, smem);
     trsm_vbatch_kernel<false><<<tot, threads, smem, s>>>(dp, ds, (int)keep.size(), W);
   }
   post_launch();

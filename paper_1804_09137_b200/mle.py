@@ -31,12 +31,20 @@ class TraceEntry:
 
 @dataclass
 class EstimationResult:
+    """stats.py:82-93 (+ `evaluations`, the objective calls made)."""
+
     theta_hat: MaternParams
     loglik: float
     iterations: int
     converged: bool
     evaluations: int
     trace: list = field(repr=False, default_factory=list)
+    mode: str = "dense"
+    accuracy: float | None = None
+
+    @property
+    def total_seconds(self) -> float:
+        return sum(t.seconds for t in self.trace)
 
 
 class EstimationError(Exception):
@@ -140,8 +148,12 @@ def mle_fit(locs, z, cfg: LikelihoodConfig, objective=None, max_evaluations: int
     except _Budget:
         pass
     if best["x"] is None or not math.isfinite(best["f"]):
-        last = trace[-1].theta if trace else tuple(float(v) for v in x0)
+        # the reference reports the simplex's best vertex (stats.py:238-240)
+        if len(vals) == len(pts) and pts:
+            last = tuple(float(v) for v in pts[int(np.argmin(vals))])
+        else:
+            last = tuple(float(v) for v in x0)
         raise EstimationError(last)
     x = best["x"]
     return EstimationResult(MaternParams(x[0], x[1], x[2], cfg.nugget), -best["f"], it, converged,
-                            len(trace), trace)
+                            len(trace), trace, mode=cfg.mode, accuracy=cfg.accuracy)

@@ -69,26 +69,46 @@ class OracleOps:
         return sla.solve_triangular(L, b, lower=True)
 
 
-class GlooComm:
-    def __init__(self):
-        self.rank = dist.get_rank()
+class GlooGroup:
+    """One communicator (world, a process row or a process column) over a
+    gloo group; members are numbered by their position in `ranks`."""
+
+    def __init__(self, ranks, group):
+        self.ranks, self.group = list(ranks), group
 
     def bcast(self, obj, root):
         box = [obj]
-        dist.broadcast_object_list(box, src=root)
+        dist.broadcast_object_list(box, src=self.ranks[root], group=self.group)
         return box[0]
 
     def reduce_sum(self, vec, root):
         import torch
         t = torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64))
-        dist.reduce(t, dst=root, op=dist.ReduceOp.SUM)
+        dist.reduce(t, dst=self.ranks[root], op=dist.ReduceOp.SUM, group=self.group)
         return t.numpy()
 
-    def allreduce_sum(self, x):
+    def allreduce_sum(self, vec):
         import torch
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t)
-        return float(t.item())
+        t = torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64))
+        dist.all_reduce(t, group=self.group)
+        return t.numpy()
+
+
+class GlooComm:
+    """World + process-row + process-column communicators of a P x Q grid
+    (every rank creates every group, in the same order)."""
+
+    def __init__(self, P, Q):
+        self.rank = dist.get_rank()
+        world = P * Q
+        self.world = GlooGroup(range(world), None)
+        rows = [[p * Q + q for q in range(Q)] for p in range(P)]
+        cols = [[p * Q + q for p in range(P)] for q in range(Q)]
+        rg = [dist.new_group(r) for r in rows]
+        cg = [dist.new_group(c) for c in cols]
+        p, q = self.rank // Q, self.rank % Q
+        self.row = GlooGroup(rows[p], rg[p])
+        self.col = GlooGroup(cols[q], cg[q])
 
 
 def _worker(rank, world, port, acc, out):
@@ -97,13 +117,13 @@ def _worker(rank, world, port, acc, out):
     xy = orc.generate_locations(N, 5)
     z = np.random.default_rng(3).standard_normal(N)
     P, Q = grid_shape(world)
-    ll, ld, q = dist_loglik(N, -(-N // NB), orc.tile_bounds(N, NB), z, OracleOps(xy, acc), GlooComm(),
+    ll, ld, q = dist_loglik(N, -(-N // NB), orc.tile_bounds(N, NB), z, OracleOps(xy, acc), GlooComm(P, Q),
                             BlockCyclic(P, Q), acc)
     out[rank] = (ll, ld, q)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("acc", [None, 1e-7])
 def test_block_cyclic_matches_single_process(world, acc):
     port = 29500 + world * 7 + (0 if acc is None else 3)
@@ -127,8 +147,18 @@ def test_layout_balance_and_messages():
     cnt = lay.balance(83)            # C3 tile grid
     assert max(cnt) / min(cnt) < 1.3   # lower-triangle block-cyclic: diagonal ranks carry more
     msgs = lay.step_messages(5, 83)
-    assert msgs[0] == ("L", (5, 5), lay.owner(5, 5)) and len(msgs) == 78
-    assert all(0 <= root < 8 for _, _, root in msgs)
+    assert msgs[0] == ("col", 5 % 4, 5 % 2, ((5, 5),))
+    # every panel tile reaches the owners of its tile row (row step) and of
+    # its tile column (column step)
+    row_tiles = {tl for c, _, _, ts in msgs if c == "row" for tl in ts}
+    assert row_tiles == {(i, 5) for i in range(6, 83)}
+    col_msgs = [(q, p, ts) for c, q, p, ts in msgs[1:] if c == "col"]
+    assert {tl for _, _, ts in col_msgs for tl in ts} == {(j, 5) for j in range(6, 83)}
+    for q, p, ts in col_msgs:
+        assert all(j % 4 == q and j % 2 == p for j, _ in ts)
+    # one packed message per process row and per non-empty (column, root row):
+    # with P = 2 | Q = 4, j mod 4 fixes j mod 2, so 4 column messages
+    assert len(msgs) == 1 + 2 + 4
     seen = set()
     for i in range(20):
         for j in range(i + 1):
