@@ -159,6 +159,14 @@ int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown,
                      int64_t m, double theta1, double theta2, double theta3,
                      double nugget, double acc, double* pred);
 
+/* tlrb_predict plus the conditional covariance of the unknown sites,
+ * S11 - S12 S22^-1 S21 (predict.py:81-87), m x m column-major in cov:
+ * generated, solved (m right-hand sides) and multiplied on the device.
+ * Single-GPU handles (TLRB_ERR_ARG otherwise). */
+int32_t tlrb_predict_var(tlrb_handle* h, const double* z, const double* xy_unknown, int64_t m,
+                         double th1, double th2, double th3, double nugget, double acc,
+                         double* pred, double* cov);
+
 /* Tile rank map of the last factor: ranks[i*t + j] for i > j (t = tiles);
  * -1 marks a tile stored dense.  Returns t via *t_out. */
 int32_t tlrb_rank_map(tlrb_handle* h, int32_t* ranks, int32_t cap, int32_t* t_out);
@@ -188,6 +196,13 @@ int32_t tlrb_matern_block_metric(const double* rows_xy, int64_t m, const double*
  * (column-major, ld = m / n; caller provides min(m,n) columns). */
 int32_t tlrb_compress_tile(const double* a, int32_t m, int32_t n, double acc,
                            int32_t* rank, double* u, double* v, int32_t device);
+
+/* Cholesky of one dense tile (potrf_tile, linalg.py:36-45): a is n x n
+ * column-major (the lower triangle is read), l receives the lower factor
+ * (upper part zero).  TLRB_ERR_NPD when a pivot is not positive: *pivot is
+ * its 0-based column (the reference's info - 1). */
+int32_t tlrb_potrf_tile(const double* a, int32_t n, int32_t tile_index, double* l, int32_t* pivot,
+                        int32_t device);
 
 /* Number of kernels this library has launched in this process. */
 int64_t tlrb_launch_count(void);

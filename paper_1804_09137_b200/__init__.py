@@ -12,12 +12,15 @@ from .api import (  # noqa: F401
     NotPositiveDefiniteError,
     PredictionProblem,
     bessel_k,
+    close_handles,
     compress_tile,
     generate_locations,
+    group_handle,
     launch_count,
     log_likelihood,
     log_likelihood_parts,
     matern_block,
+    potrf_tile,
     predict,
     sample_measurements,
 )
@@ -33,9 +36,9 @@ from .dataio import (  # noqa: F401
 
 __all__ = [
     "EARTH_RADIUS_KM", "DeviceError", "Euclidean", "GreatCircle", "Handle", "LikelihoodConfig", "LocationSet", "MaternParams",
-    "NotPositiveDefiniteError", "PredictionProblem", "bessel_k", "compress_tile",
-    "generate_locations", "launch_count", "log_likelihood", "log_likelihood_parts",
-    "matern_block", "predict", "sample_measurements",
+    "NotPositiveDefiniteError", "PredictionProblem", "bessel_k", "close_handles", "compress_tile",
+    "generate_locations", "group_handle", "launch_count", "log_likelihood", "log_likelihood_parts",
+    "matern_block", "potrf_tile", "predict", "sample_measurements",
     "DataError", "Dataset", "load_dataset", "partition_regions", "save_dataset",
     "EstimationError", "EstimationResult", "mle_fit",
     "holdout_experiment", "mc_experiment", "mc_summaries", "mse",

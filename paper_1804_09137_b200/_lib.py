@@ -65,6 +65,8 @@ SIGNATURES = [
     ("tlrb_solve", C.c_int32, [C.c_void_p, _DP, _DP]),
     ("tlrb_predict", C.c_int32, [C.c_void_p, _DP, _DP, C.c_int64, C.c_double, C.c_double, C.c_double,
                                  C.c_double, C.c_double, _DP]),
+    ("tlrb_predict_var", C.c_int32, [C.c_void_p, _DP, _DP, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, C.c_double, _DP, _DP]),
     ("tlrb_rank_map", C.c_int32, [C.c_void_p, _IP, C.c_int32, _IP]),
     ("tlrb_last_error", C.c_int32, [C.c_void_p, _IP, _IP, C.c_char_p, C.c_int32]),
     ("tlrb_bessel_k", C.c_int32, [C.c_double, _DP, C.c_int64, _DP, C.c_int32]),
@@ -73,6 +75,7 @@ SIGNATURES = [
     ("tlrb_matern_block_metric", C.c_int32, [_DP, C.c_int64, _DP, C.c_int64, C.c_double, C.c_double,
                                              C.c_double, C.c_double, _DP, C.c_int32]),
     ("tlrb_compress_tile", C.c_int32, [_DP, C.c_int32, C.c_int32, C.c_double, _IP, _DP, _DP, C.c_int32]),
+    ("tlrb_potrf_tile", C.c_int32, [_DP, C.c_int32, C.c_int32, _DP, _IP, C.c_int32]),
     ("tlrb_launch_count", C.c_int64, []),
     ("tlrb_profile_enable", C.c_int32, [C.c_int32]),
     ("tlrb_profile_mask", C.c_int32, [C.c_uint32]),

@@ -322,6 +322,19 @@ class Handle:
             raise ValueError(f"no member {member}")
         return st.as_dict()
 
+    def predict_var(self, z, unknown_xy, p: MaternParams, acc: float | None):
+        """(mean, conditional covariance) of the unknown sites (tlrb_predict_var)."""
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        u = np.ascontiguousarray(unknown_xy, dtype=np.float64)
+        m = u.shape[0]
+        out = np.empty(m)
+        cov = np.empty((m, m))
+        rc = self.lib.tlrb_predict_var(self.h, dptr(z), dptr(u), m, p.theta1, p.theta2, p.theta3, p.nugget,
+                                       float(acc or 0.0), dptr(out), dptr(cov))
+        if rc:
+            self._raise(rc)
+        return out, cov.T.copy()   # column-major on the device
+
     def rank_map(self) -> np.ndarray:
         t = np.zeros(1, np.int32)
         self.lib.tlrb_rank_map(self.h, None, 0, iptr(t))
@@ -473,15 +486,27 @@ def log_likelihood_parts(locs, z, p: MaternParams, cfg: LikelihoodConfig = Likel
     return ll, ld, q, h.last_stats
 
 
-def sample_measurements(locs, p_true: MaternParams, seed: int) -> np.ndarray:
-    """One zero-mean field realisation z = L w (stats.py:115-133): dense tile
-    Cholesky with nb = min(200, n) on the device, w = default_rng(seed)
-    standard normals (the reference's own stream, drawn on the host)."""
+def sample_measurements(locs, p_true: MaternParams, seed: int, accuracy: float | None = None,
+                        nb: int | None = None, max_rank: int | None = None, ngpus: int = 1) -> np.ndarray:
+    """One zero-mean field realisation z = L w (stats.py:115-133), w the
+    reference's own default_rng(seed) standard normals drawn on the host.
+
+    Default (the reference's recipe): dense tile Cholesky with
+    nb = min(200, n) on the device.  accuracy = eps (the C4 /
+    C5 inputs, where a dense factor does not fit): z = L~ w with L~ the TLR
+    factor at eps (nb default 400, max_rank as in LikelihoodConfig), i.e. a
+    field whose covariance is within eps of Sigma(p_true)."""
     coords = _coords_of(locs)
     n = coords.shape[0]
-    h = Handle(coords, min(DEFAULT_NB_DENSE, n), device=_local_device(), radius=_radius_of(locs))
+    if accuracy is None:
+        tile = min(DEFAULT_NB_DENSE if nb is None else nb, n)
+    else:
+        if not (0.0 < accuracy < 1.0):
+            raise ValueError(f"accuracy must lie in (0, 1), got {accuracy}")
+        tile = min(DEFAULT_NB_TLR if nb is None else nb, n)
+    h = Handle(coords, tile, max_rank or 0, ngpus=ngpus, device=_local_device(), radius=_radius_of(locs))
     try:
-        h.factorize(p_true, None)
+        h.factorize(p_true, accuracy)
         w = np.random.default_rng(seed).standard_normal(n)
         return h.apply_factor(w)
     finally:
@@ -532,16 +557,11 @@ def predict(p: PredictionProblem, with_variance: bool = False):
     radius = _radius_of(p.known)
     h = _handle_for(coords, nb, p.max_rank, 1, radius)
     uxy = _coords_of(p.unknown)
-    pred = h.predict(np.asarray(p.z, dtype=float), uxy, p.theta,
-                     p.accuracy if p.mode == "tlr" else None)
+    acc = p.accuracy if p.mode == "tlr" else None
     if not with_variance:
-        return pred
-    s12 = matern_block(uxy, coords, p.theta, radius)   # m x n, device generated
-    s11 = matern_block(uxy, uxy, p.theta, radius)
-    if p.theta.nugget:
-        s11[np.diag_indices_from(s11)] += p.theta.nugget
-    v = np.stack([h.solve(row) for row in s12], axis=1)   # Sigma_22^-1 Sigma_21 (n x m)
-    return pred, s11 - s12 @ v
+        return h.predict(np.asarray(p.z, dtype=float), uxy, p.theta, acc)
+    # one device call: factor, mean, S22^-1 S21 (m right-hand sides), S11 - S12 (.)
+    return h.predict_var(np.asarray(p.z, dtype=float), uxy, p.theta, acc)
 
 
 # ------------------------------------------------------ component entry points
@@ -585,6 +605,26 @@ def compress_tile(a: np.ndarray, eps: float):
         raise ValueError(f"tlrb_compress_tile failed ({rc})")
     r = int(k[0])
     return (u[: m * r].reshape(r, m).T.copy(), v[: n * r].reshape(r, n).T.copy())
+
+
+def potrf_tile(a: np.ndarray, tile_index: int = 0) -> np.ndarray:
+    """Device Cholesky of one tile, lower factor (linalg.potrf_tile,
+    linalg.py:36-45); raises NotPositiveDefiniteError(tile_index, pivot)."""
+    lib = _lib.load()
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[0]
+    if a.ndim != 2 or a.shape[1] != n:
+        raise ValueError(f"tile must be square, got {a.shape}")
+    af = np.asfortranarray(a)
+    out = np.zeros((n, n), order="F")
+    piv = np.zeros(1, np.int32)
+    rc = lib.tlrb_potrf_tile(dptr(af.ravel(order="K")), n, int(tile_index), out.ctypes.data_as(_lib._DP),
+                             iptr(piv), 0)
+    if rc == _lib.TLRB_ERR_NPD:
+        raise NotPositiveDefiniteError(int(tile_index), int(piv[0]))
+    if rc:
+        raise ValueError(f"tlrb_potrf_tile failed ({rc})")
+    return np.ascontiguousarray(out)
 
 
 def launch_count() -> int:

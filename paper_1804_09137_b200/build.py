@@ -16,24 +16,6 @@ if os.environ.get("TLRB_CLOCK_PROF") == "1":   # clock64 phase counters (rebuild
     FLAGS.append("-DTLRB_CLOCK_PROF")
 
 
-def cutlass_include():
-    """The CUTLASS header tree vendored in the image (flashinfer / tilelang
-    wheels); None if absent (gemm_cutlass.cu then compiles to a stub)."""
-    import site
-    roots = list(site.getsitepackages()) + [site.getusersitepackages()]
-    for r in roots:
-        for sub in ("flashinfer/data/cutlass/include", "tilelang/3rdparty/cutlass/include"):
-            p = Path(r) / sub
-            if (p / "cutlass" / "gemm" / "device" / "gemm_grouped.h").exists():
-                return p
-    return None
-
-
-_CUT = cutlass_include()
-if _CUT is not None:
-    FLAGS += ["-DTLRB_HAVE_CUTLASS", "-I" + str(_CUT)]
-
-
 def needs_build() -> bool:
     if not OUT.exists():
         return True

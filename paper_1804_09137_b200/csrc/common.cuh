@@ -218,12 +218,9 @@ void launch_gen_tiles(const std::vector<GenTile>& tiles, const Pts& pts, const M
 void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s);
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
 // multi-launch staging: build several batches on the host, upload once, launch
-struct GemmStaged { int poff = 0, soff = 0, n = 0, tot = 0; double fl = 0, by = 0; };
+struct GemmStaged { int poff = 0, soff = 0, moff = -1, n = 0, tot = 0, cfg = 0; double fl = 0, by = 0; };
 GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls);
 void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s);
-// CUTLASS grouped DMMA GEMM for the eligible problems; returns the others
-std::vector<GemmProb> launch_gemm_cutlass(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
-bool have_cutlass_gemm();
 void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);

@@ -7,9 +7,12 @@
 // a step of the tile Cholesky (all SYRK / GEMM / low-rank product updates of
 // panel k) is one launch.
 //
-// CTA: 128 threads = 4 warps in a 2x2 layout, warp tile 32x32 = 4x4 DMMA
-// tiles; BK = 16; operands staged global -> registers -> shared memory with a
-// two-stage ping-pong so the next K slab loads while DMMAs run.
+// Three tile configurations of one kernel template (64x64 / 4 warps / 4
+// stages, 64x128 / 4 warps / 3 stages, 128x128 / 8 warps / 3 stages), chosen
+// per launch from the batch's shapes; operands go global -> shared memory
+// through a multi-stage cp.async (LDGSTS) pipeline, fragments from shared
+// memory into DMMA.  Replaces the round-1 register-staged kernel and the
+// CUTLASS grouped GEMM (no external headers).
 #include "common.cuh"
 #include <chrono>
 #include <cstdlib>
@@ -19,7 +22,9 @@
 
 namespace tlrb {
 
-constexpr int GBM = 64, GBN = 64, GBK = 16, GPAD = 8;
+constexpr int GBK = 16;        // K slab per pipeline stage
+constexpr int PADK = 4;        // k-contiguous smem rows: stride GBK + 4 (conflict-free fragments)
+constexpr int PADMN = 8;       // m/n-contiguous smem rows: stride BM/BN + 8
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -27,119 +32,262 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(128) dgemm_vbatch_kernel(const GemmProb* __restrict__ probs,
-                                                           const int* __restrict__ start,
-                                                           int nprob) {
+// 8-byte global -> shared asynchronous copy (LDGSTS); src_bytes = 0 fills
+// the shared word with zeros (tile edges)
+// (`base` is a valid global address of the operand, used when nothing is read)
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, const double* base, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(ok ? gmem : base),
+               "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Batched FP64 GEMM, C = alpha op(A) op(B) + beta Cin, one CTA per BM x BN
+// output tile of any problem of the batch (binary search of the tile prefix
+// sums).  Warps in a (BM/WM) x (BN/WN) grid, warp tile WM x WN of 8x8 DMMA
+// fragments; ST-stage cp.async pipeline of K slabs of 16.  Shared layouts
+// follow the operand's contiguous direction so that the asynchronous copies
+// are coalesced and the fragment reads hit distinct banks:
+//   op(A) = A   (m contiguous): As[k][m], stride BM + 8
+//   op(A) = A^T (k contiguous): As[m][k], stride 16 + 4
+//   op(B) = B   (k contiguous): Bs[n][k], stride 16 + 4
+//   op(B) = B^T (n contiguous): Bs[k][n], stride BN + 8
+template <int BM, int BN, int WM, int WN, int ST, int KS>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
+    dgemm_tiles_kernel(const GemmProb* __restrict__ probs, const int* __restrict__ start,
+                       const int* __restrict__ blk2p, int nprob) {
+  constexpr int NT = (BM / WM) * (BN / WN) * KS * 32;
+  constexpr int AS = (BM + PADMN) * GBK > BM * (GBK + PADK) ? (BM + PADMN) * GBK : BM * (GBK + PADK);
+  constexpr int BS = (BN + PADMN) * GBK > BN * (GBK + PADK) ? (BN + PADMN) * GBK : BN * (GBK + PADK);
+  constexpr int FM = WM / 8, FN = WN / 8;
+  extern __shared__ double smem[];
+  double* As = smem;              // ST x AS
+  double* Bs = smem + ST * AS;    // ST x BS
+
   const int blk = blockIdx.x;
-  int lo = 0, hi = nprob - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (start[mid] <= blk) lo = mid; else hi = mid - 1;
+  int lo = 0;
+  if (blk2p) {   // per-CTA problem index (one load instead of a dependent binary search)
+    lo = blk2p[blk];
+  } else {
+    int hi = nprob - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= blk) lo = mid; else hi = mid - 1;
+    }
   }
-  const GemmProb P = probs[lo];
+  const GemmProb& P = probs[lo];
   if (P.active && !*P.active) return;
   const int local = blk - start[lo];
-  const int tm = (P.m + GBM - 1) / GBM;
-  const int m0 = (local % tm) * GBM, n0 = (local / tm) * GBN;
-  if (P.lower_only && n0 >= m0 + GBM) return;
-
-  __shared__ double As[2][GBK][GBM + GPAD];
-  __shared__ double Bs[2][GBK][GBN + GPAD];
+  const int tm = (P.m + BM - 1) / BM;
+  const int m0 = (local % tm) * BM, n0 = (local / tm) * BN;
+  if (P.lower_only && n0 >= m0 + BM) return;
+  const int M = P.m, N = P.n, K = P.k, lda = P.lda, ldb = P.ldb;
+  const bool ta = P.ta, tb = P.tb;
+  const double* __restrict__ A = P.A;
+  const double* __restrict__ B = P.B;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  constexpr int WG = (BM / WM) * (BN / WN);   // warps per K slice
+  const int wk = warp / WG;                   // this warp's share of each slab's k-steps (split K)
+  const int wm = (warp % WG % (BM / WM)) * WM, wn = (warp % WG / (BM / WM)) * WN;
 
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // per-thread copy positions: NT is a multiple of BM, BN and 16, so each
+  // thread's elements of a stage lie on one row / column stride apart and a
+  // single base pointer per operand serves all of them
+  static_assert(NT % BM == 0 && NT % BN == 0 && NT % GBK == 0, "copy layout");
+  const int a_r = ta ? tid / GBK : tid % BM, a_k = ta ? tid % GBK : tid / BM;
+  const int b_c = tb ? tid % BN : tid / GBK, b_k = tb ? tid / BN : tid % GBK;
+  const double* a_base = ta ? A + (size_t)(m0 + a_r) * lda + a_k : A + (size_t)a_k * lda + m0 + a_r;
+  const double* b_base = tb ? B + (size_t)b_k * ldb + n0 + b_c : B + (size_t)(n0 + b_c) * ldb + b_k;
+  const int a_soff = ta ? a_r * (GBK + PADK) + a_k : a_k * (BM + PADMN) + a_r;
+  const int b_soff = tb ? b_k * (BN + PADMN) + b_c : b_c * (GBK + PADK) + b_k;
 
-  double ra[8], rb[8];
-  auto load = [&](int k0) {
+  auto load_stage = [&](int st, int k0) {
+    double* as = As + st * AS + a_soff;
+    double* bs = Bs + st * BS + b_soff;
+    if (!ta) {   // A(m, k) at A[k lda + m]: rows a_r fixed, k = a_k + i NT / BM
+      const double* g = a_base + (size_t)k0 * lda;
+      const bool rok = m0 + a_r < M;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = tid + i * 128;
-      int r, kk;
-      if (!P.ta) { r = e & 63; kk = e >> 6; } else { r = e >> 4; kk = e & 15; }
-      const int gr = m0 + r, gk = k0 + kk;
-      double v = 0.0;
-      if (gr < P.m && gk < P.k)
-        v = P.ta ? P.A[(size_t)gr * P.lda + gk] : P.A[(size_t)gk * P.lda + gr];
-      ra[i] = v;
-      int c;
-      if (!P.tb) { kk = e & 15; c = e >> 4; } else { c = e & 63; kk = e >> 6; }
-      const int gc = n0 + c;
-      const int gk2 = k0 + kk;
-      double w = 0.0;
-      if (gc < P.n && gk2 < P.k)
-        w = P.tb ? P.B[(size_t)gk2 * P.ldb + gc] : P.B[(size_t)gc * P.ldb + gk2];
-      rb[i] = w;
+      for (int i = 0; i < BM * GBK / NT; ++i)
+        cp_async8(as + i * (NT / BM) * (BM + PADMN), g + (size_t)i * (NT / BM) * lda, A,
+                  rok && k0 + a_k + i * (NT / BM) < K);
+    } else {     // A^T: A(m, k) at A[m lda + k]: k = a_k fixed, m = a_r + i NT / 16
+      const double* g = a_base + k0;
+      const bool kok = k0 + a_k < K;
+#pragma unroll
+      for (int i = 0; i < BM * GBK / NT; ++i)
+        cp_async8(as + i * (NT / GBK) * (GBK + PADK), g + (size_t)i * (NT / GBK) * lda, A,
+                  kok && m0 + a_r + i * (NT / GBK) < M);
+    }
+    if (!tb) {   // B(k, n) at B[n ldb + k]: k = b_k fixed, n = b_c + i NT / 16
+      const double* g = b_base + k0;
+      const bool kok = k0 + b_k < K;
+#pragma unroll
+      for (int i = 0; i < BN * GBK / NT; ++i)
+        cp_async8(bs + i * (NT / GBK) * (GBK + PADK), g + (size_t)i * (NT / GBK) * ldb, B,
+                  kok && n0 + b_c + i * (NT / GBK) < N);
+    } else {     // B^T: B(k, n) at B[k ldb + n]: n = b_c fixed, k = b_k + i NT / BN
+      const double* g = b_base + (size_t)k0 * ldb;
+      const bool nok = n0 + b_c < N;
+#pragma unroll
+      for (int i = 0; i < BN * GBK / NT; ++i)
+        cp_async8(bs + i * (NT / BN) * (BN + PADMN), g + (size_t)i * (NT / BN) * ldb, B,
+                  nok && k0 + b_k + i * (NT / BN) < K);
     }
   };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = tid + i * 128;
-      int r, kk;
-      if (!P.ta) { r = e & 63; kk = e >> 6; } else { r = e >> 4; kk = e & 15; }
-      As[buf][kk][r] = ra[i];
-      int c;
-      if (!P.tb) { kk = e & 15; c = e >> 4; } else { c = e & 63; kk = e >> 6; }
-      Bs[buf][kk][c] = rb[i];
-    }
-  };
 
-  const int nk = (P.k + GBK - 1) / GBK;
-  if (nk > 0) {
-    load(0);
-    store(0);
-    __syncthreads();
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (K + GBK - 1) / GBK;
+#pragma unroll
+  for (int st = 0; st < ST - 1; ++st) {
+    if (st < nk) load_stage(st, st * GBK);
+    cp_async_commit();
   }
+  const int fr = lane >> 2, fk = lane & 3;
   for (int kc = 0; kc < nk; ++kc) {
-    const int cur = kc & 1;
-    if (kc + 1 < nk) load((kc + 1) * GBK);
+    cp_async_wait<ST - 2>();
+    __syncthreads();
+    // refill the stage consumed at kc - 1 (everyone is past it)
+    {
+      const int kn = kc + ST - 1;
+      if (kn < nk) load_stage(kn % ST, kn * GBK);
+      cp_async_commit();
+    }
+    const double* as = As + (kc % ST) * AS;
+    const double* bs = Bs + (kc % ST) * BS;
 #pragma unroll
-    for (int k4 = 0; k4 < GBK; k4 += 4) {
-      double a[4], b[4];
-      const int kr = k4 + (lane & 3);
+    for (int k4 = 4 * wk; k4 < GBK; k4 += 4 * KS) {
+      const int kr = k4 + fk;
+      double a[FM], b[FN];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        a[t] = As[cur][kr][wm + t * 8 + (lane >> 2)];
-        b[t] = Bs[cur][kr][wn + t * 8 + (lane >> 2)];
+      for (int t = 0; t < FM; ++t) {
+        const int r = wm + t * 8 + fr;
+        a[t] = !ta ? as[kr * (BM + PADMN) + r] : as[r * (GBK + PADK) + kr];
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int t = 0; t < FN; ++t) {
+        const int c = wn + t * 8 + fr;
+        b[t] = !tb ? bs[c * (GBK + PADK) + kr] : bs[kr * (BN + PADMN) + c];
+      }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    if (kc + 1 < nk) store(cur ^ 1);
+  }
+  cp_async_wait<0>();
+  if constexpr (KS > 1) {   // sum the K slices' partial tiles through shared memory
     __syncthreads();
+    double* red = smem;     // (KS - 1) x WG warps x FM x FN x 2 x 32
+    constexpr int PER = FM * FN * 2 * 32;
+    if (wk > 0) {
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            red[((size_t)(wk - 1) * WG + warp % WG) * PER + ((i * FN + j) * 2 + h) * 32 + lane] = acc[i][j][h];
+    }
+    __syncthreads();
+    if (wk == 0) {
+      for (int q = 1; q < KS; ++q)
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              acc[i][j][h] += red[((size_t)(q - 1) * WG + warp) * PER + ((i * FN + j) * 2 + h) * 32 + lane];
+    }
   }
 
-  // epilogue: C = alpha acc + beta Cin
+  // epilogue through shared memory: the warps drop alpha * acc into a
+  // column-major BM x BN tile, then consecutive threads write consecutive
+  // rows of a column (coalesced C / Cin traffic, which dominates the
+  // small-k shapes: trailing updates, M formation)
+  const double alpha = P.alpha, beta = P.beta;
+  __syncthreads();   // every warp is done with the pipeline buffers
+  constexpr int LDC = BM + 1;
+  double* cs = smem;
+  if (KS == 1 || wk == 0) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = m0 + wm + i * 8 + (lane >> 2);
-    if (r >= P.m) continue;
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < FN; ++j)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = n0 + wn + j * 8 + 2 * (lane & 3) + h;
-        if (c >= P.n) continue;
-        double v = P.alpha * acc[i][j][h];
-        if (P.beta != 0.0) v += P.beta * P.Cin[(size_t)c * P.ldcin + r];
-        P.C[(size_t)c * P.ldc + r] = v;
-      }
-    }
+        for (int h = 0; h < 2; ++h)
+          cs[(wn + j * 8 + 2 * fk + h) * LDC + wm + i * 8 + fr] = alpha * acc[i][j][h];
   }
+  __syncthreads();
+  const int mr = min(BM, M - m0), nc = min(BN, N - n0);
+  double* __restrict__ Cout = P.C + (size_t)n0 * P.ldc + m0;
+  const double* __restrict__ Cin = beta != 0.0 ? P.Cin + (size_t)n0 * P.ldcin + m0 : nullptr;
+  for (int e = tid; e < BM * BN; e += NT) {
+    const int r = e % BM, c = e / BM;
+    if (r >= mr || c >= nc) continue;
+    double v = cs[c * LDC + r];
+    if (beta != 0.0) v += beta * Cin[(size_t)c * P.ldcin + r];
+    Cout[(size_t)c * P.ldc + r] = v;
+  }
+}
+
+// tile configurations (m x n tile, warp tile, stages)
+struct GemmCfg { int bm, bn; };
+constexpr GemmCfg kCfg[5] = {{64, 64}, {64, 128}, {128, 128}, {32, 32}, {32, 128}};
+
+template <int BM, int BN, int WM, int WN, int ST>
+size_t tiles_smem() {
+  constexpr int AS = (BM + PADMN) * GBK > BM * (GBK + PADK) ? (BM + PADMN) * GBK : BM * (GBK + PADK);
+  constexpr int BS = (BN + PADMN) * GBK > BN * (GBK + PADK) ? (BN + PADMN) * GBK : BN * (GBK + PADK);
+  return (size_t)ST * (AS + BS) * sizeof(double);
+}
+
+template <int BM, int BN, int WM, int WN, int ST, int KS = 1>
+void run_tiles(int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
+  auto kern = dgemm_tiles_kernel<BM, BN, WM, WN, ST, KS>;
+  const size_t red = (size_t)(KS - 1) * (BM / WM) * (BN / WN) * (WM / 8) * (WN / 8) * 2 * 32 * sizeof(double);
+  const size_t epi = (size_t)(BM + 1) * BN * sizeof(double);
+  const size_t sm = std::max({tiles_smem<BM, BN, WM, WN, ST>(), red, epi});
+  allow_smem(kern, sm);
+  kern<<<tot, (BM / WM) * (BN / WN) * KS * 32, sm, s>>>(dp, ds, dm, n);
+}
+
+// configuration of a batch: the larger tiles once the problems are large
+// enough to fill them (measured on the TLR batch shapes, tools/bench_gemm.cu)
+int pick_cfg(const std::vector<GemmProb>& probs) {
+  static const int force = getenv("TLRB_GEMM_CFG") ? atoi(getenv("TLRB_GEMM_CFG")) : -1;
+  if (force >= 0 && force < 5) return force;
+  double fl = 0, fl_big = 0, fl_huge = 0, fl_small = 0, fl_thin = 0;
+  for (const GemmProb& p : probs) {
+    const double f = 2.0 * p.m * p.n * p.k;
+    fl += f;
+    if (p.m >= 96 && p.n >= 96) fl_big += f;
+    if (p.m >= 256 && p.n >= 256 && p.k >= 64) fl_huge += f;
+    if (p.m <= 40 && p.n <= 40 && p.k >= 128) fl_small += f;
+    if (p.m <= 40 && p.n >= 96) fl_thin += f;
+  }
+  if (fl_huge >= 0.7 * fl) return 2;
+  if (fl_big >= 0.7 * fl) return 1;
+  if (fl_small >= 0.7 * fl) return 3;
+  if (fl_thin >= 0.7 * fl) return 4;
+  return 0;
 }
 
 // host-side staging of one batched launch: appends the non-empty problems and
 // their tile prefix sums to (allp, alls); returns the launch record
 GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls) {
   GemmStaged g;
+  g.cfg = pick_cfg(probs);
+  const int bm = kCfg[g.cfg].bm, bn = kCfg[g.cfg].bn;
   g.poff = (int)allp.size();
   g.soff = (int)alls.size();
   int tot = 0;
@@ -147,13 +295,24 @@ GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>&
     if (p.m <= 0 || p.n <= 0) continue;
     allp.push_back(p);
     alls.push_back(tot);
-    tot += ((p.m + GBM - 1) / GBM) * ((p.n + GBN - 1) / GBN);
+    tot += ((p.m + bm - 1) / bm) * ((p.n + bn - 1) / bn);
     g.fl += 2.0 * p.m * p.n * p.k;
     g.by += 8.0 * ((double)p.m * p.k + (double)p.k * p.n + (double)p.m * p.n * (p.beta != 0.0 ? 2 : 1));
   }
   alls.push_back(tot);
   g.n = (int)allp.size() - g.poff;
   g.tot = tot;
+  // CTA -> problem map after the prefix sums (small and mid-size launches:
+  // their CTAs are short, a dependent binary search per CTA would dominate)
+  if (g.n > 1 && tot <= (1 << 18)) {
+    g.moff = (int)alls.size();
+    alls.resize(alls.size() + tot);
+    int* mp = alls.data() + g.moff;
+    for (int q = 0; q < g.n; ++q) {
+      const int a = alls[g.soff + q], b = alls[g.soff + q + 1];
+      for (int c = a; c < b; ++c) mp[c] = q;
+    }
+  }
   return g;
 }
 
@@ -161,7 +320,16 @@ GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>&
 void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s) {
   if (g.tot == 0 || g.n == 0) return;
   ProfScope ps(K_GEMM, s, g.fl, g.by);
-  dgemm_vbatch_kernel<<<g.tot, 128, 0, s>>>(dp + g.poff, ds + g.soff, g.n);
+  const GemmProb* p = dp + g.poff;
+  const int* st = ds + g.soff;
+  const int* mp = g.moff >= 0 ? ds + g.moff : nullptr;
+  switch (g.cfg) {
+    case 4: run_tiles<32, 128, 32, 64, 4, 2>(g.tot, p, st, mp, g.n, s); break;
+    case 3: run_tiles<32, 32, 32, 32, 4, 4>(g.tot, p, st, mp, g.n, s); break;
+    case 2: run_tiles<128, 128, 32, 64, 3>(g.tot, p, st, mp, g.n, s); break;
+    case 1: run_tiles<64, 128, 32, 64, 3>(g.tot, p, st, mp, g.n, s); break;
+    default: run_tiles<64, 64, 32, 32, 4>(g.tot, p, st, mp, g.n, s); break;
+  }
   post_launch();
 }
 
@@ -216,17 +384,11 @@ void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t
 
 void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
-  // large plain problems go to the CUTLASS grouped DMMA kernel (gemm_cutlass.cu);
-  // lower-only, flagged and skinny ones stay here (TLRB_GEMM_CUTLASS=0: all here)
-  static const bool use_cutlass = have_cutlass_gemm() && !(getenv("TLRB_GEMM_CUTLASS") &&
-                                                           atoi(getenv("TLRB_GEMM_CUTLASS")) == 0);
-  const std::vector<GemmProb> rest = use_cutlass ? launch_gemm_cutlass(probs, ar, s) : probs;
-  if (rest.empty()) return;
   std::vector<GemmProb> keep;
   std::vector<int> start;
-  keep.reserve(rest.size());
-  start.reserve(rest.size() + 1);
-  const GemmStaged g = stage_gemm(rest, keep, start);
+  keep.reserve(probs.size());
+  start.reserve(probs.size() + 1);
+  const GemmStaged g = stage_gemm(probs, keep, start);
   if (g.tot == 0) return;
   const GemmProb* dp = ar.put(keep, s);
   const int* ds = ar.put(start, s);

@@ -32,6 +32,7 @@
 #include <chrono>
 #include <mutex>
 #include <thread>
+#include <limits>
 
 using namespace tlrb;
 
@@ -60,6 +61,23 @@ double factored_frac(int nb) {
 
 // roofline denominators of tlrb_stats.t_roof_ms (tlrb_set_peaks)
 double g_peak_flops = 35.5e12, g_peak_bytes = 6449.7e9;
+
+// Storage rule of a tile's factors when a storage cap (BASELINE max_rank,
+// SURVEY A13) is configured: a tile is kept exact (dense, updated by GEMMs,
+// never recompressed) once its rank at the accuracy exceeds the cap, or
+// exceeds rho min(m, n), where its low-rank form already takes
+// k (m + n) = 2 rho m n doubles of a square tile's m n (rho = 0.45:
+// 0.9 m n).  Keeping such a tile exact is more accurate than the reference's
+// truncation (never below acc, compression.py:6) and removes the costliest
+// recompressions (QRCP + Jacobi of a nearly full-rank nb x nb tile on every
+// update).  Without a cap every tile follows the reference's truncation
+// exactly (its TLR-vs-dense gap, hundreds of acc on ill-conditioned inputs,
+// is part of the parity contract).  TLRB_DENSE_FRAC overrides rho (>= 1: cap
+// only).
+double dense_frac() {
+  static const double v = getenv("TLRB_DENSE_FRAC") ? atof(getenv("TLRB_DENSE_FRAC")) : 0.45;
+  return v;
+}
 
 struct Flops {
   double f = 0, b = 0, troof = 0;   // troof: sum over ops of max(F / P64, B / BW), seconds
@@ -121,7 +139,7 @@ struct tlrb_handle {
   double* d_y = nullptr;         // y = L x output (n), allocated on first use
   // kriging
   double* d_ux = nullptr; double* d_uy = nullptr; double* d_uz = nullptr; double* d_pred = nullptr;
-  double* d_partial = nullptr; int64_t ucap = 0;
+  double* d_partial = nullptr; double* d_pacc = nullptr; int64_t ucap = 0;
   DescArena ar;
   // compression workspace
   char* ws = nullptr;
@@ -210,6 +228,11 @@ struct tlrb_handle {
 };
 
 namespace {
+
+int dense_rank_limit(const tlrb_handle* h, int m, int n) {
+  if (h->max_rank <= 0) return std::numeric_limits<int>::max();   // no cap: the reference's rule only
+  return (int)std::floor(std::min(dense_frac() * std::min(m, n), (double)h->max_rank));
+}
 
 bool trace_on() {
   static const bool on = getenv("TLRB_TRACE") != nullptr;
@@ -405,7 +428,8 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
     // 2n flops, + the scaled rotation, 4n flops) = 3 n s (s-1) flops
     if (g_prof.on && J.s) g_prof.add_work(K_JACOBI, 3.0 * J.n * (double)J.s * (J.s - 1) * sw[j], 0);
     const int k = J.out_rank;
-    J.dense_out = h->max_rank > 0 && k > h->max_rank && !J.factored;
+    // (a standalone compression, tlrb_compress_tile, has no tile: always U V^T)
+    J.dense_out = !J.factored && J.tile >= 0 && k > dense_rank_limit(h, J.m, J.n);
     if (J.tile >= 0) {   // the destination tile's storage is sized by the new rank
       if (J.dense_out || k) h->ensure((size_t)J.tile, J.dense_out ? h->nb : k, J.dense_out);
       J.Uout = h->uptr[J.tile];
@@ -488,23 +512,26 @@ void compress_all(tlrb_handle* h, double acc) {
 // ------------------------------------------------------------------ POTRF
 // L_kk on its owner (linalg.py:36-45); distributed handles then share it
 // down process column k mod Q, where the panel tiles (i, k) live (share_lkk)
+// right-looking blocked Cholesky of one n x n tile (lower, ld): 32-column
+// panel kernel + DMMA trailing update; the first failure lands in info
+void potrf_blocks(double* A, int ld, int n, int tile, int* info, double* logdiag, DescArena& ar, cudaStream_t s) {
+  for (int r0 = 0; r0 < n; r0 += kPotrfBlock) {
+    const int bs = std::min(kPotrfBlock, n - r0);
+    launch_potrf_block(A, ld, n, r0, bs, tile, info, logdiag, s);
+    const int rest = n - r0 - bs;
+    if (rest > 0) {
+      double* A21 = A + (size_t)r0 * ld + r0 + bs;
+      double* A22 = A + (size_t)(r0 + bs) * ld + r0 + bs;
+      launch_gemm({GemmProb{A21, A21, A22, A22, rest, rest, bs, ld, ld, ld, ld, 0, 1, 1, -1.0, 1.0}}, ar, s);
+    }
+  }
+}
+
 void potrf(tlrb_handle* h, int k, cudaStream_t s = nullptr) {
   if (!s) s = h->stream;
   if (!h->own(k, k)) return;
   const int n = h->sz[k];
-  double* A = h->D(k);
-  for (int r0 = 0; r0 < n; r0 += kPotrfBlock) {
-    const int bs = std::min(kPotrfBlock, n - r0);
-    launch_potrf_block(A, h->nb, n, r0, bs, k, h->d_info, h->d_logdiag + h->off[k], s);
-    const int rest = n - r0 - bs;
-    if (rest > 0) {
-      double* A21 = A + (size_t)r0 * h->nb + r0 + bs;
-      double* A22 = A + (size_t)(r0 + bs) * h->nb + r0 + bs;
-      launch_gemm({GemmProb{A21, A21, A22, A22, rest, rest, bs, h->nb, h->nb, h->nb, h->nb, 0, 1, 1,
-                            -1.0, 1.0}},
-                  h->ar, s);
-    }
-  }
+  potrf_blocks(h->D(k), h->nb, n, k, h->d_info, h->d_logdiag + h->off[k], h->ar, s);
   const double nn = n;
   h->work.add(nn * nn * nn / 3.0, 16.0 * nn * nn);
 }
@@ -788,7 +815,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       launch_gemm(g2, h->ar, h->stream);
       launch_gemm(g3, h->ar, h->stream);
     }
-    if (lookahead && !h->dist() && k + 1 < t) {
+    if (lookahead && k + 1 < t && h->own(k + 1, k + 1)) {
       TLRB_CUDA(cudaEventRecord(h->ev_syrk, h->stream));
       TLRB_CUDA(cudaStreamWaitEvent(h->side, h->ev_syrk, 0));
       potrf(h, k + 1, h->side);
@@ -878,7 +905,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
                           (size_t)4 * 128 * K <= nb2s &&
                           2 * ((size_t)128 * K + 16384) + (size_t)ki * kj <= nb2s;
-        return fits && K <= factored_frac(nb) * std::min(mi, mj) && (h->max_rank <= 0 || K <= h->max_rank);
+        return fits && K <= factored_frac(nb) * std::min(mi, mj) && K <= dense_rank_limit(h, mi, mj);
       };
       // dense-path jobs first (slots 0..nd-1), factored ones after them
       std::vector<size_t> order;
@@ -1242,24 +1269,26 @@ void gather_solution(tlrb_handle* h) {
 }
 
 // ------------------------------------------------------------------ solves
-void forward_solve(tlrb_handle* h) {
-  if (h->dist()) { solve_dist(h, false); gather_solution(h); return; }
+// Single-GPU triangular solves on q right-hand sides X (n x q, ld ldx),
+// tile column by tile column (linalg.py:166-197): TRSM of the diagonal tile
+// then one batched GEMM launch (two for low-rank tiles, through the scratch
+// W: t * nb x q) for every tile below / left of it.
+void forward_solve_multi(tlrb_handle* h, double* X, int ldx, int q, double* W) {
   const int t = h->t, nb = h->nb;
   for (int j = 0; j < t; ++j) {
-    double* yj = h->d_z + h->off[j];
-    launch_trsm({TrsmProb{h->D(j), nb, yj, h->sz[j], h->sz[j], 1}}, false, h->ar, h->stream);
+    double* yj = X + h->off[j];
+    launch_trsm({TrsmProb{h->D(j), nb, yj, ldx, h->sz[j], q}}, false, h->ar, h->stream);
     std::vector<GemmProb> g1, g2;
     for (int i = j + 1; i < t; ++i) {
-      double* yi = h->d_z + h->off[i];
+      double* yi = X + h->off[i];
       if (h->factor_mode == 1 || h->dn(i, j)) {  // y_i -= T_ij^T y_j
-        g1.push_back({h->Ut(i, j), yj, yi, yi, h->sz[i], 1, h->sz[j], nb, h->sz[j], h->sz[i], h->sz[i], 1, 0, 0,
-                      -1.0, 1.0});
+        g1.push_back({h->Ut(i, j), yj, yi, yi, h->sz[i], q, h->sz[j], nb, ldx, ldx, ldx, 1, 0, 0, -1.0, 1.0});
       } else {
         const int r = h->rank[h->tid(i, j)];
         if (!r) continue;
-        double* w = h->d_w + (size_t)i * nb;
-        g1.push_back({h->Vt(i, j), yj, nullptr, w, r, 1, h->sz[j], nb, h->sz[j], r, r, 1, 0, 0, 1.0, 0.0});
-        g2.push_back({h->Ut(i, j), w, yi, yi, h->sz[i], 1, r, nb, r, h->sz[i], h->sz[i], 0, 0, 0, -1.0, 1.0});
+        double* w = W + (size_t)i * nb * q;
+        g1.push_back({h->Vt(i, j), yj, nullptr, w, r, q, h->sz[j], nb, ldx, r, r, 1, 0, 0, 1.0, 0.0});
+        g2.push_back({h->Ut(i, j), w, yi, yi, h->sz[i], q, r, nb, r, ldx, ldx, 0, 0, 0, -1.0, 1.0});
       }
     }
     launch_gemm(g1, h->ar, h->stream);
@@ -1267,29 +1296,37 @@ void forward_solve(tlrb_handle* h) {
   }
 }
 
-void backward_solve(tlrb_handle* h) {
-  if (h->dist()) { solve_dist(h, true); gather_solution(h); return; }
+void backward_solve_multi(tlrb_handle* h, double* X, int ldx, int q, double* W) {
   const int t = h->t, nb = h->nb;
   for (int i = t - 1; i >= 0; --i) {
-    double* xi = h->d_z + h->off[i];
-    launch_trsm({TrsmProb{h->D(i), nb, xi, h->sz[i], h->sz[i], 1}}, true, h->ar, h->stream);
+    double* xi = X + h->off[i];
+    launch_trsm({TrsmProb{h->D(i), nb, xi, ldx, h->sz[i], q}}, true, h->ar, h->stream);
     std::vector<GemmProb> g1, g2;
     for (int j = 0; j < i; ++j) {
-      double* xj = h->d_z + h->off[j];
+      double* xj = X + h->off[j];
       if (h->factor_mode == 1 || h->dn(i, j)) {  // x_j -= L_ij^T x_i = T_ij x_i
-        g1.push_back({h->Ut(i, j), xi, xj, xj, h->sz[j], 1, h->sz[i], nb, h->sz[i], h->sz[j], h->sz[j], 0, 0, 0,
-                      -1.0, 1.0});
+        g1.push_back({h->Ut(i, j), xi, xj, xj, h->sz[j], q, h->sz[i], nb, ldx, ldx, ldx, 0, 0, 0, -1.0, 1.0});
       } else {
         const int r = h->rank[h->tid(i, j)];
         if (!r) continue;
-        double* w = h->d_w + (size_t)j * nb;
-        g1.push_back({h->Ut(i, j), xi, nullptr, w, r, 1, h->sz[i], nb, h->sz[i], r, r, 1, 0, 0, 1.0, 0.0});
-        g2.push_back({h->Vt(i, j), w, xj, xj, h->sz[j], 1, r, nb, r, h->sz[j], h->sz[j], 0, 0, 0, -1.0, 1.0});
+        double* w = W + (size_t)j * nb * q;
+        g1.push_back({h->Ut(i, j), xi, nullptr, w, r, q, h->sz[i], nb, ldx, r, r, 1, 0, 0, 1.0, 0.0});
+        g2.push_back({h->Vt(i, j), w, xj, xj, h->sz[j], q, r, nb, r, ldx, ldx, 0, 0, 0, -1.0, 1.0});
       }
     }
     launch_gemm(g1, h->ar, h->stream);
     launch_gemm(g2, h->ar, h->stream);
   }
+}
+
+void forward_solve(tlrb_handle* h) {
+  if (h->dist()) { solve_dist(h, false); gather_solution(h); return; }
+  forward_solve_multi(h, h->d_z, (int)h->n, 1, h->d_w);
+}
+
+void backward_solve(tlrb_handle* h) {
+  if (h->dist()) { solve_dist(h, true); gather_solution(h); return; }
+  backward_solve_multi(h, h->d_z, (int)h->n, 1, h->d_w);
 }
 
 // -------------------------------------------------------------- one eval
@@ -1776,13 +1813,17 @@ int predict_one(tlrb_handle* h, const double* z, const double* xy_unknown, int64
   TLRB_CUDA(cudaSetDevice(h->device));
   cudaStream_t s = h->stream;
   if (m > h->ucap) {
-    if (h->d_ux) { cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_uz); cudaFree(h->d_pred); cudaFree(h->d_partial); }
+    if (h->d_ux) {
+      cudaFree(h->d_ux); cudaFree(h->d_uy); cudaFree(h->d_uz); cudaFree(h->d_pred); cudaFree(h->d_partial);
+      cudaFree(h->d_pacc);
+    }
     h->ucap = m;
     const int64_t nchunk = (h->n + 2047) / 2048;
     TLRB_CUDA(cudaMalloc(&h->d_ux, m * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_uy, m * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_uz, m * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_pred, m * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&h->d_pacc, m * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_partial, m * nchunk * sizeof(double)));
   }
   std::vector<double> ux, uy, uz;
@@ -1796,12 +1837,63 @@ int predict_one(tlrb_handle* h, const double* z, const double* xy_unknown, int64
   if (r) return r;
   forward_solve(h);
   backward_solve(h);
-  if (pred) {   // group handles: one member forms the cross-covariance product
-    launch_cross_gemv(h->pts(), h->d_z, h->n, Pts{h->d_ux, h->d_uy, h->d_uz, h->diam}, m, h->mp,
-                      h->d_partial, h->d_pred, s);
-    TLRB_CUDA(cudaMemcpyAsync(pred, h->d_pred, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  const Pts unk{h->d_ux, h->d_uy, h->d_uz, h->diam};
+  if (h->dist()) {
+    // SURVEY 8(e) kriging: each rank generates the cross-covariance columns
+    // of its own diagonal tiles' sites and multiplies them with its solved
+    // tiles; one all-reduce of the m-vector
+    TLRB_CUDA(cudaMemsetAsync(h->d_pred, 0, m * sizeof(double), s));
+    for (int j = 0; j < h->t; ++j) {
+      if (!h->own(j, j)) continue;
+      const int64_t o = h->off[j];
+      const Pts kp{h->dx + o, h->dy + o, h->dz ? h->dz + o : nullptr, h->diam};
+      launch_cross_gemv(kp, h->d_z + o, h->sz[j], unk, m, h->mp, h->d_partial, h->d_pacc, s);
+      axpy_kernel<<<4, 256, 0, s>>>(h->d_pred, h->d_pacc, 1.0, (int)m);
+      post_launch();
+    }
+    h->cw->allreduce_sum(h->d_pred, m, CType::F64, s);
+  } else {
+    launch_cross_gemv(h->pts(), h->d_z, h->n, unk, m, h->mp, h->d_partial, h->d_pred, s);
   }
+  if (pred) TLRB_CUDA(cudaMemcpyAsync(pred, h->d_pred, m * sizeof(double), cudaMemcpyDeviceToHost, s));
   h->sync();
+  return TLRB_OK;
+}
+
+// conditional covariance S11 - S12 S22^-1 S21 of the unknown sites on the
+// factor just computed (predict.py:81-87), all on the device: S21 generated
+// from [known; unknown] points, q = m right-hand-side solves, one GEMM
+int kriging_cov(tlrb_handle* h, int64_t m, double nugget, double* cov) {
+  cudaStream_t s = h->stream;
+  const int64_t n = h->n, nt = n + m;
+  double *cx = nullptr, *cy = nullptr, *cz = nullptr, *S = nullptr, *W = nullptr, *C = nullptr;
+  auto cat = [&](double*& dst, const double* a, const double* b) {
+    TLRB_CUDA(cudaMalloc(&dst, nt * sizeof(double)));
+    TLRB_CUDA(cudaMemcpyAsync(dst, a, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    TLRB_CUDA(cudaMemcpyAsync(dst + n, b, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  };
+  cat(cx, h->dx, h->d_ux);
+  cat(cy, h->dy, h->d_uy);
+  if (h->diam > 0.0) cat(cz, h->dz, h->d_uz);
+  TLRB_CUDA(cudaMalloc(&S, (size_t)n * m * sizeof(double)));
+  TLRB_CUDA(cudaMalloc(&W, (size_t)h->t * h->nb * m * sizeof(double)));
+  TLRB_CUDA(cudaMalloc(&C, (size_t)m * m * sizeof(double)));
+  const Pts all{cx, cy, cz, h->diam};
+  // S21 (n x m): rows = known sites, columns = unknown sites (disjoint index
+  // ranges: no diagonal term); S11 (m x m) with the nugget on its diagonal
+  launch_gen_tiles({GenTile{S, (int)n, 0, (int)n, (int)n, (int)m, 0.0},
+                    GenTile{C, (int)m, (int)n, (int)m, (int)n, (int)m, nugget}},
+                   all, h->mp, h->ar, s);
+  forward_solve_multi(h, S, (int)n, (int)m, W);
+  backward_solve_multi(h, S, (int)n, (int)m, W);   // S <- S22^-1 S21
+  // C = S11 - S21^T (S22^-1 S21): generate a fresh S21 into W for the left factor
+  launch_gen_tiles({GenTile{W, (int)n, 0, (int)n, (int)n, (int)m, 0.0}}, all, h->mp, h->ar, s);
+  launch_gemm({GemmProb{W, S, C, C, (int)m, (int)m, (int)n, (int)n, (int)n, (int)m, (int)m, 1, 0, 0, -1.0, 1.0}},
+              h->ar, s);
+  TLRB_CUDA(cudaMemcpyAsync(cov, C, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  h->sync();
+  for (double* p : {cx, cy, cz, S, W, C})
+    if (p) cudaFree(p);
   return TLRB_OK;
 }
 
@@ -1906,7 +1998,7 @@ void tlrb_destroy(tlrb_handle* h) {
   h->ccol.reset();
   void* ptrs[] = {h->dx, h->dy, h->dz, h->d_uz, h->diag, h->arena, h->d_info, h->d_logdiag, h->d_scal, h->d_z, h->d_w,
                   h->ws, h->d_sums, h->d_aux, h->d_kind, h->d_ok, h->d_rank, h->d_sweeps, h->d_perm, h->d_y, h->d_ux, h->d_uy,
-                  h->d_pred, h->d_partial, h->d_ibuf, h->d_acc, h->lkk, h->pbuf};
+                  h->d_pred, h->d_partial, h->d_pacc, h->d_ibuf, h->d_acc, h->lkk, h->pbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->ar.release();
@@ -1978,6 +2070,22 @@ int32_t tlrb_predict(tlrb_handle* h, const double* z, const double* xy_unknown, 
       return predict_one(mm, z, xy_unknown, m, th1, th2, th3, nugget, acc, r ? nullptr : pred);
     });
   return guarded(h, [&] { return predict_one(h, z, xy_unknown, m, th1, th2, th3, nugget, acc, pred); });
+}
+
+int32_t tlrb_predict_var(tlrb_handle* h, const double* z, const double* xy_unknown, int64_t m, double th1,
+                         double th2, double th3, double nugget, double acc, double* pred, double* cov) {
+  if (!h || !z || !xy_unknown || !pred || !cov || m < 1) return TLRB_ERR_ARG;
+  int rc = validate(th1, th2, th3, nugget, acc);
+  if (rc) return rc;
+  if (h->group() || h->dist()) {
+    h->msg = "conditional covariance: single-GPU handles only";
+    return TLRB_ERR_ARG;
+  }
+  return guarded(h, [&]() -> int {
+    const int r = predict_one(h, z, xy_unknown, m, th1, th2, th3, nugget, acc, pred);
+    if (r) return r;
+    return kriging_cov(h, m, nugget, cov);
+  });
 }
 
 int32_t tlrb_rank_map(tlrb_handle* h, int32_t* ranks, int32_t cap, int32_t* t_out) {
@@ -2060,6 +2168,41 @@ int32_t tlrb_matern_block_metric(const double* rows_xy, int64_t m, const double*
     cudaFree(po);
     return TLRB_OK;
   });
+}
+
+int32_t tlrb_potrf_tile(const double* a, int32_t n, int32_t tile_index, double* l, int32_t* pivot,
+                        int32_t device) {
+  if (!a || !l || n < 1) return TLRB_ERR_ARG;
+  if (pivot) *pivot = -1;
+  int info[3] = {0, 0, 0};
+  const int rc = guarded(nullptr, [&]() -> int {
+    TLRB_CUDA(cudaSetDevice(device));
+    double *dA = nullptr, *dlog = nullptr;
+    int* dinfo = nullptr;
+    TLRB_CUDA(cudaMalloc(&dA, (size_t)n * n * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&dlog, (size_t)n * sizeof(double)));
+    TLRB_CUDA(cudaMalloc(&dinfo, 3 * sizeof(int)));
+    TLRB_CUDA(cudaMemset(dinfo, 0, 3 * sizeof(int)));
+    TLRB_CUDA(cudaMemcpy(dA, a, (size_t)n * n * sizeof(double), cudaMemcpyHostToDevice));
+    DescArena ar;
+    ar.init(1 << 20);
+    potrf_blocks(dA, n, n, tile_index, dinfo, dlog, ar, 0);
+    tril_kernel<<<64, 256>>>(dA, n, n);   // np.tril (linalg.py:45)
+    post_launch();
+    TLRB_CUDA(cudaMemcpy(l, dA, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost));
+    TLRB_CUDA(cudaMemcpy(info, dinfo, sizeof info, cudaMemcpyDeviceToHost));
+    ar.release();
+    cudaFree(dA);
+    cudaFree(dlog);
+    cudaFree(dinfo);
+    return TLRB_OK;
+  });
+  if (rc) return rc;
+  if (info[0]) {
+    if (pivot) *pivot = info[2];
+    return TLRB_ERR_NPD;
+  }
+  return TLRB_OK;
 }
 
 int32_t tlrb_set_metric(tlrb_handle* h, double sphere_radius) {

@@ -89,7 +89,14 @@ def test_loglik_tlr_parity(tb, gold, name):
             h = tb.api._handle_for(locs.coords, min(e["nb"], e["n"]), None, 1)
             rm = h.rank_map()
             ref = r["factor_ranks"]
-            diff = sum(1 for k, v in ref.items() if rm[tuple(map(int, k.split(",")))] != v)
+            nbm = min(e["nb"], e["n"])
+            diff = 0
+            for k, v in ref.items():
+                got = rm[tuple(map(int, k.split(",")))]
+                if got == -1:   # kept exact (break-even storage rule): the reference's rank is high
+                    assert v >= 0.4 * nbm, (k, v)
+                else:
+                    diff += got != v
             assert diff <= max(1, len(ref) // 50), f"{diff} of {len(ref)} factor ranks differ"
 
 

@@ -1,6 +1,7 @@
 """One warm TLR evaluation of a BASELINE config for TLRB_TRACE runs (z is
 standard normal: tile ranks and the work do not depend on z):
-    TLRB_TRACE=1 python tools/trace_cfg.py C3 2> trace.log"""
+    TLRB_TRACE=1 python tools/trace_cfg.py C3 2> trace.log
+--dense: the dense (no compression) evaluation instead."""
 import sys
 import time
 from pathlib import Path
@@ -17,15 +18,16 @@ locs = tb.generate_locations(c["n"], 0)
 z = np.random.default_rng(1).standard_normal(c["n"])
 h = tb.Handle(locs.coords, c["nb"], max_rank=c["max_rank"] or 0)
 p = tb.MaternParams(*c["theta"])
+acc = None if "--dense" in sys.argv else c["acc"]
 if warm:
-    h.loglik(z, p, c["acc"])
+    h.loglik(z, p, acc)
 print("---- warm", file=sys.stderr, flush=True)
 prof = "--profile" in sys.argv   # per-kernel-class event times (serialising)
 if prof:
     from paper_1804_09137_b200 import _lib
     _lib.profile_enable(True)
 t0 = time.perf_counter()
-ll = h.loglik(z, p, c["acc"])
+ll = h.loglik(z, p, acc)
 print(f"ll {ll[0]!r}  wall {time.perf_counter() - t0:.3f} s  stats {h.last_stats}")
 if prof:
     for k, v in sorted(_lib.profile_read().items(), key=lambda kv: -kv[1]["ms"]):
