@@ -36,9 +36,12 @@ def test_library_is_sm100a():
 def test_dmma_in_sass():
     so = ROOT / "paper_1804_09137_b200" / "libtlrb200.so"
     out = subprocess.run(["cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
-    # the FP64 GEMM issues mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4 (16 per k4 step, unrolled)
-    sec = out.split("dgemm_vbatch_kernel", 1)[1].split("Function :", 1)[0]
-    assert sec.count("DMMA") >= 64
+    # the FP64 GEMM issues mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; every tile
+    # configuration of the template must carry it
+    secs = [f.split("Function :", 1)[0] for f in out.split("dgemm_tiles_kernel")[1:]]
+    assert len(secs) >= 5
+    for sec in secs:
+        assert sec.count("DMMA") >= 16
 
 
 def test_generate_locations_matches_oracle(tb):
