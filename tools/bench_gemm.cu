@@ -11,6 +11,7 @@
 #include <vector>
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
 
 using namespace tlrb;
 
@@ -38,7 +39,10 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (const Shape& sh : shapes) {
+  const int only = getenv("BENCH_SHAPE") ? atoi(getenv("BENCH_SHAPE")) : -1;   // one shape (ncu captures)
+  for (size_t si = 0; si < shapes.size(); ++si) {
+    if (only >= 0 && (int)si != only) continue;
+    const Shape& sh = shapes[si];
     const int lda = sh.ta ? sh.k : sh.m, ldb = sh.tb ? sh.n : sh.k, ldc = sh.m;
     const size_t sa = (size_t)lda * (sh.ta ? sh.m : sh.k), sb = (size_t)ldb * (sh.tb ? sh.k : sh.n),
                  sc = (size_t)ldc * sh.n;

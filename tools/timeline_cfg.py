@@ -1,6 +1,6 @@
-"""Kernel timeline of one warm C2 TLR evaluation (TLRB_TIMELINE dump of the
-per-launch CUDA events): busy/idle time, per-class union, 10 ms buckets.
-    python tools/timeline_c2.py [acc]"""
+"""Kernel timeline of one warm TLR evaluation (TLRB_TIMELINE dump of the
+per-launch CUDA events): busy/idle time, per-class union, time buckets.
+    python tools/timeline_cfg.py C3 [acc] [--bucket MS]"""
 import os
 import sys
 import tempfile
@@ -15,11 +15,16 @@ os.environ["TLRB_TIMELINE"] = path
 import paper_1804_09137_b200 as tb  # noqa: E402
 from paper_1804_09137_b200 import _lib  # noqa: E402
 
-acc = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-9
-locs = tb.generate_locations(10000, 0)
-z = np.load(ROOT / "tests/golden/z_big.npz")["C2"]
-h = tb.Handle(locs.coords, 500)
-p = tb.MaternParams(1.0, 0.1, 0.5)
+from tools.run_config import CONFIGS  # noqa: E402
+
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+cfg = CONFIGS[args[0] if args else "C2"]
+acc = float(args[1]) if len(args) > 1 else cfg["acc"]
+B = float(sys.argv[sys.argv.index("--bucket") + 1]) if "--bucket" in sys.argv else 10.0
+locs = tb.generate_locations(cfg["n"], 0)
+z = np.random.default_rng(1).standard_normal(cfg["n"])
+h = tb.Handle(locs.coords, cfg["nb"], max_rank=cfg["max_rank"] or 0)
+p = tb.MaternParams(*cfg["theta"])
 h.loglik(z, p, acc)
 if os.path.exists(path):
     os.remove(path)
@@ -51,8 +56,7 @@ print(f"span {end - t0:.1f} ms  busy(any kernel) {busy:.1f} ms  idle {end - t0 -
 for c in sorted({c for _, _, c in ev}):
     iv = [(a, b) for a, b, cc in ev if cc == c]
     print(f"  {c:16s} union {union(iv):8.1f} ms  sum {sum(b - a for a, b in iv):8.1f} ms  n {len(iv)}")
-# 10 ms buckets: fraction of time each class is active
-B = 10.0
+# buckets: fraction of time each class is active
 nb = int((end - t0) / B) + 1
 cls = sorted({c for _, _, c in ev})
 print("bucket(ms) " + " ".join(f"{c[:6]:>6s}" for c in cls) + "  idle")
