@@ -64,18 +64,28 @@ double g_peak_flops = 35.5e12, g_peak_bytes = 6449.7e9;
 
 // Storage rule of a tile's factors when a storage cap (BASELINE max_rank,
 // SURVEY A13) is configured: a tile is kept exact (dense, updated by GEMMs,
-// never recompressed) once its rank at the accuracy exceeds the cap, or
-// exceeds rho min(m, n), where its low-rank form already takes
-// k (m + n) = 2 rho m n doubles of a square tile's m n (rho = 0.45:
-// 0.9 m n).  Keeping such a tile exact is more accurate than the reference's
-// truncation (never below acc, compression.py:6) and removes the costliest
-// recompressions (QRCP + Jacobi of a nearly full-rank nb x nb tile on every
-// update).  Without a cap every tile follows the reference's truncation
+// never recompressed) once its QRCP rank at 1e-2 acc (an upper bound of its
+// truncation rank) exceeds the cap, or exceeds rho min(m, n).  Keeping such
+// a tile exact is more accurate than the reference's truncation (never below
+// acc, compression.py:6) and removes the costliest work of the evaluation:
+// the SVD of its initial compression and the QRCP + Jacobi of a high-rank
+// nb x nb tile on every later update.  Measured at C3 (nb = 760, cap 380,
+// tools/c3_once.py, profiles/r02_sweep.jsonl): rule on the SVD rank with
+// rho = 0.45 7.05 s; on the QRCP rank, rho = 0.45 / 0.35 / 0.3 / 0.25 / 0.2:
+// 4.99 / 4.51 / 3.95 / 3.82 / 3.81 s, likelihood 1e-8 or closer to the
+// dense one.  Without a cap every tile follows the reference's truncation
 // exactly (its TLR-vs-dense gap, hundreds of acc on ill-conditioned inputs,
-// is part of the parity contract).  TLRB_DENSE_FRAC overrides rho (>= 1: cap
-// only).
+// is part of the parity contract).  TLRB_DENSE_FRAC overrides rho (>= 1:
+// cap only).
 double dense_frac() {
-  static const double v = getenv("TLRB_DENSE_FRAC") ? atof(getenv("TLRB_DENSE_FRAC")) : 0.45;
+  static const double v = getenv("TLRB_DENSE_FRAC") ? atof(getenv("TLRB_DENSE_FRAC")) : 0.25;
+  return v;
+}
+
+// TLRB_DENSE_BY_QRCP=0: decide exact storage on the SVD truncation rank only
+// (the SVD of every capped tile runs); default: on the QRCP rank
+bool dense_by_qrcp() {
+  static const bool v = !(getenv("TLRB_DENSE_BY_QRCP") && atoi(getenv("TLRB_DENSE_BY_QRCP")) == 0);
   return v;
 }
 
@@ -364,14 +374,20 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
   }
   const double t_q1 = trace_on() ? now_ms() : 0;
   std::vector<int> kinds(nj);
+  // under a storage cap, a tile whose QRCP rank already exceeds the dense
+  // limit is kept exact without its SVD: the truncation rank never exceeds
+  // the QRCP rank (the Jacobi tail only shrinks it), and an exact tile is
+  // never less accurate than the truncated one (see dense_frac)
+  std::vector<char> pre_dense(nj, 0);
   {
     std::vector<CopyProb> cp;
     for (int j = 0; j < nj; ++j) {
       Job& J = jobs[j];
       J.s = rr[j];
       kinds[j] = 1 | (J.kind & 2);   // e2 = QRCP residual (sums[6j+1])
+      pre_dense[j] = dense_by_qrcp() && !J.factored && J.tile >= 0 && J.s > dense_rank_limit(h, J.m, J.n);
       // X (n x r): X(p, c) = R(c, p) for p >= c
-      if (J.s)
+      if (J.s && !pre_dense[j])
         cp.push_back({J.M, J.m, J.Bt, J.n, J.n, J.s, 1, 1.0, 1, nullptr,
                       gathered[j] ? d_perm + (size_t)j * h->nb : nullptr});
     }
@@ -383,6 +399,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
     std::vector<JacobiProb> jp;
     for (int j = 0; j < nj; ++j) {
       Job& J = jobs[j];
+      if (pre_dense[j]) continue;   // d_rank keeps the QRCP rank (> the dense limit)
       jp.push_back({J.Bt, J.n, J.Vs, J.n, J.sig, d_aux + 3 * j, acc, d_rank + j,
                     d_sweeps + j, J.n, J.s});
     }
@@ -394,7 +411,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
       for (auto& q : jp) q.prof = nullptr;
       jp[0].prof = d_prof;   // first problem only (one tile in tools/one_tile.py)
     }
-    launch_jacobi(jp, h->ar, s);
+    if (!jp.empty()) launch_jacobi(jp, h->ar, s);
     if (prof) {
       long long hp[16 * 8];
       TLRB_CUDA(cudaMemcpyAsync(hp, d_prof, sizeof hp, cudaMemcpyDeviceToHost, s));
@@ -422,6 +439,7 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
   std::vector<CopyProb> cv;
   for (int j = 0; j < nj; ++j) {
     Job& J = jobs[j];
+    if (pre_dense[j]) sw[j] = 0;   // no SVD ran (its d_sweeps entry is stale)
     J.out_rank = J.s ? rk[j] : 0;
     h->max_sweeps = std::max(h->max_sweeps, J.s ? sw[j] : 0);
     // one-sided Jacobi as implemented: per sweep s(s-1)/2 pairs x (one dot,

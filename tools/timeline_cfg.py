@@ -17,7 +17,10 @@ from paper_1804_09137_b200 import _lib  # noqa: E402
 
 from tools.run_config import CONFIGS  # noqa: E402
 
-args = [a for a in sys.argv[1:] if not a.startswith("--")]
+argv = sys.argv[1:]
+if "--bucket" in argv:
+    del argv[argv.index("--bucket"):argv.index("--bucket") + 2]
+args = [a for a in argv if not a.startswith("--")]
 cfg = CONFIGS[args[0] if args else "C2"]
 acc = float(args[1]) if len(args) > 1 else cfg["acc"]
 B = float(sys.argv[sys.argv.index("--bucket") + 1]) if "--bucket" in sys.argv else 10.0
