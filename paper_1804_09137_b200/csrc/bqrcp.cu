@@ -622,9 +622,16 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
   while (true) {
     // stage the GEMM descriptors of the next `planned` blocks in one upload
     const int it0 = it;
-    const int nit = std::max(0, std::min(planned, (kmax_all + b - 1) / b - it0));
+    int nit = std::max(0, std::min(planned, (kmax_all + b - 1) / b - it0));
     allp.clear(); alls.clear(); rec.clear();
+    // the staged descriptors of one upload stay within a fixed budget (large
+    // tiles: nb = 1900 stages ~0.6 MB per block for a 24 x 24 tile grid)
+    constexpr size_t kStageBudget = 12u << 20;
     for (int q = 0; q < nit; ++q) {
+      if (q > 0 && allp.size() * sizeof(GemmProb) + alls.size() * sizeof(int) > kStageBudget) {
+        nit = q;
+        break;
+      }
       const int j = (it0 + q) * b;
       g0.clear(); g1.clear(); g2.clear(); g3.clear();
       for (int p = 0; p < np; ++p) {
@@ -691,7 +698,7 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
     bool any = false;
     for (const BqState& x : hs) any |= x.active != 0;
     if (!any) break;
-    planned = 3;
+    planned = std::max(3, planned - nit);   // the rest of the prediction, then three blocks at a time
   }
 }
 

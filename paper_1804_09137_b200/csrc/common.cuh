@@ -28,9 +28,17 @@ struct CudaError {
   }
 };
 
+// TLRB_SYNC_CHECK=1 (diagnostic): synchronise after every launch and, on an
+// error, print the host call stack of the launch that produced it
+bool sync_check_on();
+void sync_check_fail();
 inline void post_launch() {
   ++g_launches;
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && sync_check_on()) {
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) sync_check_fail();
+  }
   if (e != cudaSuccess) throw CudaError(e, "kernel launch", __FILE__, __LINE__);
 }
 
@@ -218,7 +226,7 @@ void launch_gen_tiles(const std::vector<GenTile>& tiles, const Pts& pts, const M
 void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s);
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
 // multi-launch staging: build several batches on the host, upload once, launch
-struct GemmStaged { int poff = 0, soff = 0, moff = -1, n = 0, tot = 0, cfg = 0; double fl = 0, by = 0; };
+struct GemmStaged { int poff = 0, soff = 0, moff = -1, n = 0, tot = 0, cfg = 0; double fl = 0, by = 0; bool vec = false; };
 GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls);
 void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s);
 void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);

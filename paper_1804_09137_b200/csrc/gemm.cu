@@ -40,6 +40,13 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, cons
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(ok ? gmem : base),
                "r"(ok ? 8 : 0));
 }
+// 16-byte variant (LDGSTS.128, L2 only): `bytes` in {0, 8, 16} are read, the
+// rest of the 16-byte shared word pair is zero-filled
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, const double* base, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(bytes ? gmem : base),
+               "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -54,7 +61,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 //   op(A) = A^T (k contiguous): As[m][k], stride 16 + 4
 //   op(B) = B   (k contiguous): Bs[n][k], stride 16 + 4
 //   op(B) = B^T (n contiguous): Bs[k][n], stride BN + 8
-template <int BM, int BN, int WM, int WN, int ST, int KS>
+template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
     dgemm_tiles_kernel(const GemmProb* __restrict__ probs, const int* __restrict__ start,
                        const int* __restrict__ blk2p, int nprob) {
@@ -95,47 +102,57 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
 
   // per-thread copy positions: NT is a multiple of BM, BN and 16, so each
   // thread's elements of a stage lie on one row / column stride apart and a
-  // single base pointer per operand serves all of them
+  // single base pointer per operand serves all of them.  VEC = 2 (every
+  // operand of the batch 16-byte aligned with an even leading dimension):
+  // a thread moves pairs along the operand's contiguous direction with one
+  // 16-byte cp.async (half the LDGSTS instructions, L1 bypassed).
   static_assert(NT % BM == 0 && NT % BN == 0 && NT % GBK == 0, "copy layout");
-  const int a_r = ta ? tid / GBK : tid % BM, a_k = ta ? tid % GBK : tid / BM;
-  const int b_c = tb ? tid % BN : tid / GBK, b_k = tb ? tid / BN : tid % GBK;
+  constexpr int CM = BM / VEC, CN = BN / VEC, CK = GBK / VEC;   // copy positions along m / n / k
+  const int a_r = ta ? tid / CK : VEC * (tid % CM), a_k = ta ? VEC * (tid % CK) : tid / CM;
+  const int b_c = tb ? VEC * (tid % CN) : tid / CK, b_k = tb ? tid / CN : VEC * (tid % CK);
   const double* a_base = ta ? A + (size_t)(m0 + a_r) * lda + a_k : A + (size_t)a_k * lda + m0 + a_r;
   const double* b_base = tb ? B + (size_t)b_k * ldb + n0 + b_c : B + (size_t)(n0 + b_c) * ldb + b_k;
   const int a_soff = ta ? a_r * (GBK + PADK) + a_k : a_k * (BM + PADMN) + a_r;
   const int b_soff = tb ? b_k * (BN + PADMN) + b_c : b_c * (GBK + PADK) + b_k;
 
+  // one copy of VEC doubles; `left` = valid elements from this position on
+  // along the contiguous direction (<= 0: nothing), `ok` = the other index
+  auto cp = [&](double* sm, const double* g, const double* base, bool ok, int left) {
+    if constexpr (VEC == 1) cp_async8(sm, g, base, ok && left > 0);
+    else cp_async16(sm, g, base, ok ? 8 * max(0, min(2, left)) : 0);
+  };
   auto load_stage = [&](int st, int k0) {
     double* as = As + st * AS + a_soff;
     double* bs = Bs + st * BS + b_soff;
-    if (!ta) {   // A(m, k) at A[k lda + m]: rows a_r fixed, k = a_k + i NT / BM
+    if (!ta) {   // A(m, k) at A[k lda + m]: rows a_r fixed, k = a_k + i NT / CM
       const double* g = a_base + (size_t)k0 * lda;
-      const bool rok = m0 + a_r < M;
+      const int left = M - (m0 + a_r);
 #pragma unroll
-      for (int i = 0; i < BM * GBK / NT; ++i)
-        cp_async8(as + i * (NT / BM) * (BM + PADMN), g + (size_t)i * (NT / BM) * lda, A,
-                  rok && k0 + a_k + i * (NT / BM) < K);
-    } else {     // A^T: A(m, k) at A[m lda + k]: k = a_k fixed, m = a_r + i NT / 16
+      for (int i = 0; i < CM * GBK / NT; ++i)
+        cp(as + i * (NT / CM) * (BM + PADMN), g + (size_t)i * (NT / CM) * lda, A,
+           k0 + a_k + i * (NT / CM) < K, left);
+    } else {     // A^T: A(m, k) at A[m lda + k]: k = a_k fixed, m = a_r + i NT / CK
       const double* g = a_base + k0;
-      const bool kok = k0 + a_k < K;
+      const int left = K - (k0 + a_k);
 #pragma unroll
-      for (int i = 0; i < BM * GBK / NT; ++i)
-        cp_async8(as + i * (NT / GBK) * (GBK + PADK), g + (size_t)i * (NT / GBK) * lda, A,
-                  kok && m0 + a_r + i * (NT / GBK) < M);
+      for (int i = 0; i < BM * CK / NT; ++i)
+        cp(as + i * (NT / CK) * (GBK + PADK), g + (size_t)i * (NT / CK) * lda, A,
+           m0 + a_r + i * (NT / CK) < M, left);
     }
-    if (!tb) {   // B(k, n) at B[n ldb + k]: k = b_k fixed, n = b_c + i NT / 16
+    if (!tb) {   // B(k, n) at B[n ldb + k]: k = b_k fixed, n = b_c + i NT / CK
       const double* g = b_base + k0;
-      const bool kok = k0 + b_k < K;
+      const int left = K - (k0 + b_k);
 #pragma unroll
-      for (int i = 0; i < BN * GBK / NT; ++i)
-        cp_async8(bs + i * (NT / GBK) * (GBK + PADK), g + (size_t)i * (NT / GBK) * ldb, B,
-                  kok && n0 + b_c + i * (NT / GBK) < N);
-    } else {     // B^T: B(k, n) at B[k ldb + n]: n = b_c fixed, k = b_k + i NT / BN
+      for (int i = 0; i < BN * CK / NT; ++i)
+        cp(bs + i * (NT / CK) * (GBK + PADK), g + (size_t)i * (NT / CK) * ldb, B,
+           n0 + b_c + i * (NT / CK) < N, left);
+    } else {     // B^T: B(k, n) at B[k ldb + n]: n = b_c fixed, k = b_k + i NT / CN
       const double* g = b_base + (size_t)k0 * ldb;
-      const bool nok = n0 + b_c < N;
+      const int left = N - (n0 + b_c);
 #pragma unroll
-      for (int i = 0; i < BN * GBK / NT; ++i)
-        cp_async8(bs + i * (NT / BN) * (BN + PADMN), g + (size_t)i * (NT / BN) * ldb, B,
-                  nok && k0 + b_k + i * (NT / BN) < K);
+      for (int i = 0; i < CN * GBK / NT; ++i)
+        cp(bs + i * (NT / CN) * (BN + PADMN), g + (size_t)i * (NT / CN) * ldb, B,
+           k0 + b_k + i * (NT / CN) < K, left);
     }
   };
 
@@ -251,14 +268,20 @@ size_t tiles_smem() {
   return (size_t)ST * (AS + BS) * sizeof(double);
 }
 
-template <int BM, int BN, int WM, int WN, int ST, int KS = 1>
-void run_tiles(int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
-  auto kern = dgemm_tiles_kernel<BM, BN, WM, WN, ST, KS>;
+template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC>
+void run_tiles_v(int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
+  auto kern = dgemm_tiles_kernel<BM, BN, WM, WN, ST, KS, VEC>;
   const size_t red = (size_t)(KS - 1) * (BM / WM) * (BN / WN) * (WM / 8) * (WN / 8) * 2 * 32 * sizeof(double);
   const size_t epi = (size_t)(BM + 1) * BN * sizeof(double);
   const size_t sm = std::max({tiles_smem<BM, BN, WM, WN, ST>(), red, epi});
   allow_smem(kern, sm);
   kern<<<tot, (BM / WM) * (BN / WN) * KS * 32, sm, s>>>(dp, ds, dm, n);
+}
+
+template <int BM, int BN, int WM, int WN, int ST, int KS = 1>
+void run_tiles(bool vec, int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
+  if (vec) run_tiles_v<BM, BN, WM, WN, ST, KS, 2>(tot, dp, ds, dm, n, s);
+  else run_tiles_v<BM, BN, WM, WN, ST, KS, 1>(tot, dp, ds, dm, n, s);
 }
 
 // configuration of a batch: the larger tiles once the problems are large
@@ -291,8 +314,13 @@ GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>&
   g.poff = (int)allp.size();
   g.soff = (int)alls.size();
   int tot = 0;
+  static const bool novec = getenv("TLRB_GEMM_NOVEC") != nullptr;
+  g.vec = !novec;
   for (const GemmProb& p : probs) {
     if (p.m <= 0 || p.n <= 0) continue;
+    // 16-byte copies need both operands 16-byte aligned with even leading dimensions
+    if (((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) || ((p.lda | p.ldb) & 1))
+      g.vec = false;
     allp.push_back(p);
     alls.push_back(tot);
     tot += ((p.m + bm - 1) / bm) * ((p.n + bn - 1) / bn);
@@ -324,11 +352,11 @@ void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, 
   const int* st = ds + g.soff;
   const int* mp = g.moff >= 0 ? ds + g.moff : nullptr;
   switch (g.cfg) {
-    case 4: run_tiles<32, 128, 32, 64, 4, 2>(g.tot, p, st, mp, g.n, s); break;
-    case 3: run_tiles<32, 32, 32, 32, 4, 4>(g.tot, p, st, mp, g.n, s); break;
-    case 2: run_tiles<128, 128, 32, 64, 3>(g.tot, p, st, mp, g.n, s); break;
-    case 1: run_tiles<64, 128, 32, 64, 3>(g.tot, p, st, mp, g.n, s); break;
-    default: run_tiles<64, 64, 32, 32, 4>(g.tot, p, st, mp, g.n, s); break;
+    case 4: run_tiles<32, 128, 32, 64, 4, 2>(g.vec, g.tot, p, st, mp, g.n, s); break;
+    case 3: run_tiles<32, 32, 32, 32, 4, 4>(g.vec, g.tot, p, st, mp, g.n, s); break;
+    case 2: run_tiles<128, 128, 32, 64, 3>(g.vec, g.tot, p, st, mp, g.n, s); break;
+    case 1: run_tiles<64, 128, 32, 64, 3>(g.vec, g.tot, p, st, mp, g.n, s); break;
+    default: run_tiles<64, 64, 32, 32, 4>(g.vec, g.tot, p, st, mp, g.n, s); break;
   }
   post_launch();
 }

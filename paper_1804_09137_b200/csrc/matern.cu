@@ -148,9 +148,14 @@ __device__ __forceinline__ double pair_dist(double diam, double p1, double p2, d
 }
 
 // ---------------------------------------------------------------- K1 tiles
-// Each CTA writes a 64 (rows) x 32 (cols) block of one tile, column-major, so
-// a warp's stores are 32 consecutive doubles (256 B, fully coalesced).
-constexpr int GEN_BM = 64, GEN_BN = 32;
+// Each CTA writes a 128 (rows) x 32 (cols) block of one tile, column-major.
+// A thread owns two consecutive rows and eight columns: its two entries of a
+// column go out as one 16-byte store (st.global.v2.f64) when the tile's
+// leading dimension and base keep the pair aligned, so a warp writes 512
+// consecutive bytes per column; the two independent K_nu evaluations per
+// column also hide the FP64 sqrt / exp latency.  Odd leading dimensions,
+// odd bases and a ragged last row fall back to 8-byte stores.
+constexpr int GEN_BM = 128, GEN_BN = 32;
 
 __global__ void __launch_bounds__(256) gen_tiles_kernel(const GenTile* __restrict__ tiles,
                                                         const int* __restrict__ start, int ntiles,
@@ -165,20 +170,32 @@ __global__ void __launch_bounds__(256) gen_tiles_kernel(const GenTile* __restric
   const int local = blk - start[lo];
   const int tm = (T.m + GEN_BM - 1) / GEN_BM;
   const int bm = local % tm, bn = local / tm;
-  const int r = bm * GEN_BM + (threadIdx.x & 63);
+  const int r = bm * GEN_BM + 2 * (threadIdx.x & 63);
   if (r >= T.m) return;
-  const int gr = T.r0 + r;
-  const double p1 = P.a1[gr], p2 = P.a2[gr], p3 = P.diam > 0.0 ? P.a3[gr] : 0.0;
+  const bool two = r + 1 < T.m;
+  const int gr = T.r0 + r, gr1 = two ? gr + 1 : gr;
+  const bool sph = P.diam > 0.0;
+  const double p1 = P.a1[gr], p2 = P.a2[gr], p3 = sph ? P.a3[gr] : 0.0;
+  const double s1 = P.a1[gr1], s2 = P.a2[gr1], s3 = sph ? P.a3[gr1] : 0.0;
+  const bool vec = two && (T.ld & 1) == 0 && ((reinterpret_cast<uintptr_t>(T.out) >> 3) + r) % 2 == 0;
   const int cbase = bn * GEN_BN + (threadIdx.x >> 6) * (GEN_BN / 4);
 #pragma unroll
   for (int cc = 0; cc < GEN_BN / 4; ++cc) {
     const int c = cbase + cc;
     if (c >= T.n) break;
     const int gc = T.c0 + c;
-    const double q3 = P.diam > 0.0 ? P.a3[gc] : 0.0;
-    double v = matern_t(p, pair_dist(P.diam, p1, p2, p3, P.a1[gc], P.a2[gc], q3) * p.inv_theta2);
-    if (gr == gc) v += T.diag_add;
-    T.out[(size_t)c * T.ld + r] = v;
+    const double q1 = P.a1[gc], q2 = P.a2[gc], q3 = sph ? P.a3[gc] : 0.0;
+    double v0 = matern_t(p, pair_dist(P.diam, p1, p2, p3, q1, q2, q3) * p.inv_theta2);
+    double v1 = matern_t(p, pair_dist(P.diam, s1, s2, s3, q1, q2, q3) * p.inv_theta2);
+    if (gr == gc) v0 += T.diag_add;
+    if (gr1 == gc) v1 += T.diag_add;
+    double* o = T.out + (size_t)c * T.ld + r;
+    if (vec) {
+      *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
+    } else {
+      o[0] = v0;
+      if (two) o[1] = v1;
+    }
   }
 }
 

@@ -2,6 +2,8 @@
 // block reductions), strided copies / transposes, seeded Gaussian sketches,
 // log-determinant and dot-product reductions, compression bookkeeping.
 #include "common.cuh"
+#include <execinfo.h>
+#include <cstdlib>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -10,6 +12,17 @@
 namespace tlrb {
 
 std::atomic<int64_t> g_launches{0};
+
+bool sync_check_on() {
+  static const bool on = getenv("TLRB_SYNC_CHECK") != nullptr;
+  return on;
+}
+void sync_check_fail() {
+  void* frames[32];
+  const int n = backtrace(frames, 32);
+  fprintf(stderr, "[tlrb] TLRB_SYNC_CHECK: launch %lld failed; host stack:\n", (long long)g_launches.load());
+  backtrace_symbols_fd(frames, n, 2);
+}
 Profiler g_prof;
 const char* kclass_name[K_NCLASS] = {"gen_tiles", "dgemm_vbatch", "trsm_vbatch", "potrf_block",
                                      "qr_householder", "jacobi_svd", "sumsq", "copy", "unused",
@@ -155,6 +168,8 @@ void DescArena::release() {
 }
 void* DescArena::put_bytes(const void* src, size_t bytes, cudaStream_t s) {
   const size_t a = (off_ + 255) & ~(size_t)255;
+  if (bytes > cap_)
+    throw CudaError(cudaErrorMemoryAllocation, "descriptor batch larger than the staging arena", __FILE__, __LINE__);
   if (a + bytes > cap_) {
     // arena full: wait until earlier descriptors are consumed (every stream
     // of the device may hold some: look-ahead / side streams)
@@ -211,8 +226,9 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyProb* __restrict__ 
   const int64_t e0 = part * per, e1 = min(tot, e0 + per);
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const int r = (int)(e % P.m), c = (int)(e / P.m);
-    double v = P.transpose ? P.src[(size_t)(P.srccol ? P.srccol[r] : r) * P.lds + c]
-                           : P.src[(size_t)c * P.lds + r];
+    double v = !P.src ? 0.0   // no source: zero fill
+               : P.transpose ? P.src[(size_t)(P.srccol ? P.srccol[r] : r) * P.lds + c]
+                             : P.src[(size_t)c * P.lds + r];
     if (P.tri && r < c) v = 0.0;
     const int rd = P.rowperm ? P.rowperm[r] : r;
     P.dst[(size_t)c * P.ldd + rd] = P.scale * v;

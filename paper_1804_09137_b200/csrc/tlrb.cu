@@ -884,7 +884,8 @@ bool factor_tlr(tlrb_handle* h, double acc) {
             dt.push_back({h->Ut(j, k), h->Ut(i, k), T, T, mj, mi, mk, nb, nb, nb, nb, 1, 0, 0, -1.0, 1.0});
           }
           const double a = di ? mk : ki, b = dj ? mk : kj;
-          h->work.add(2.0 * mi * mj * std::min(a, b) + 2.0 * mk * a * b, 8.0 * (2.0 * mi * mj + mk * (a + b)));
+          h->work.add(di && dj ? 2.0 * mi * mj * mk : 2.0 * mi * mj * std::min(a, b) + 2.0 * mk * a * b,
+                      8.0 * (2.0 * mi * mj + mk * (a + b)));
         }
       launch_gemm(dx, h->ar, h->stream);
       launch_gemm(dy, h->ar, h->stream);
@@ -1096,10 +1097,10 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           // [core factor; 0] (K x kk on top of mu - K zero rows), then Q applied in place
           fin.push_back({J.Uout, J.ldu, J.Ufin, nb, J.m, kk, 0, 1.0, 0, nullptr});
           fin.push_back({J.Vout, J.ldv, J.Vfin, nb, J.n, kk, 0, 1.0, 0, nullptr});
-          if (J.mu > J.m)
-            TLRB_CUDA(cudaMemset2DAsync(J.Ufin + J.m, (size_t)nb * 8, 0, (size_t)(J.mu - J.m) * 8, kk, h->stream));
-          if (J.nv > J.n)
-            TLRB_CUDA(cudaMemset2DAsync(J.Vfin + J.n, (size_t)nb * 8, 0, (size_t)(J.nv - J.n) * 8, kk, h->stream));
+          // zero rows below the core factor (batched zero fill: one launch
+          // for the whole batch instead of two memsets per job)
+          fin.push_back({nullptr, 0, J.Ufin + J.m, nb, J.mu - J.m, kk, 0, 1.0, 0, nullptr});
+          fin.push_back({nullptr, 0, J.Vfin + J.n, nb, J.nv - J.n, kk, 0, 1.0, 0, nullptr});
           fp.push_back(J.qu); fc.push_back(J.Ufin); fld.push_back(nb); fk.push_back(kk);
           fp.push_back(J.qv); fc.push_back(J.Vfin); fld.push_back(nb); fk.push_back(kk);
         }
@@ -1113,15 +1114,25 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       }
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
-        const double ki = h->dn(i, k) ? h->sz[k] : h->rank[h->tid(i, k)];
-        const double kj = h->dn(j, k) ? h->sz[k] : h->rank[h->tid(j, k)];
+        // algorithmic work of the update at the execution ranks:
+        // the low-rank form of L_ik L_jk^T (rank ku: the low-rank operand's
+        // when one panel tile is stored exactly, none when both are), the
+        // QRs of the stacked factors, the SVD of the K x K core and the new
+        // factors (compression.py:54-81)
+        const bool di = h->dn(i, k), dj = h->dn(j, k);
+        const double ki = h->rank[h->tid(i, k)], kj = h->rank[h->tid(j, k)], mk = h->sz[k];
         const double kij = h->dn(i, j) ? h->sz[j] : h->rank[h->tid(i, j)];
         const Job& J = jobs[posq[q - c0]];
         const double kn = J.dense_out ? h->sz[j] : J.out_rank;
-        const double K = kij + kj, Kh = std::min<double>(K, h->nb), nbd = h->sz[i];
-        h->work.add(4.0 * nbd * ki * kj + 2.0 * (4.0 * nbd * K * Kh - 4.0 / 3.0 * Kh * Kh * Kh) +
+        const double nbd = h->sz[i], nbj = h->sz[j], full = std::min(nbd, nbj);
+        const double ku = di && dj ? full : dj ? ki : kj;
+        const double prod = di && dj ? 2.0 * nbd * nbj * mk
+                            : di || dj ? 2.0 * (di ? nbd : nbj) * mk * ku
+                                       : 2.0 * mk * ki * kj + 2.0 * nbd * ki * kj;
+        const double K = std::min(kij + ku, nbd + nbj), Kh = std::min(K, full);
+        h->work.add(prod + 2.0 * (4.0 * nbd * K * Kh - 4.0 / 3.0 * Kh * Kh * Kh) +
                         24.0 * Kh * Kh * Kh + 4.0 * nbd * Kh * kn,
-                    8.0 * nbd * (2 * kij + 2 * ki + 2 * kj + 2 * kn));
+                    8.0 * (nbd + nbj) * (kij + ku + kn) + 8.0 * mk * ((di ? nbd : ki) + (dj ? nbj : kj)));
         h->rank[h->tid(i, j)] = J.dense_out ? 0 : J.out_rank;
         h->dense[h->tid(i, j)] = J.dense_out;
       }
