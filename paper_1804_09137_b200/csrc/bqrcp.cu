@@ -626,7 +626,7 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
     allp.clear(); alls.clear(); rec.clear();
     // the staged descriptors of one upload stay within a fixed budget (large
     // tiles: nb = 1900 stages ~0.6 MB per block for a 24 x 24 tile grid)
-    constexpr size_t kStageBudget = 12u << 20;
+    const size_t kStageBudget = std::min<size_t>(12u << 20, ar.capacity() / 4);
     for (int q = 0; q < nit; ++q) {
       if (q > 0 && allp.size() * sizeof(GemmProb) + alls.size() * sizeof(int) > kStageBudget) {
         nit = q;
@@ -664,6 +664,9 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
       rec.push_back(stage_gemm(g2, allp, alls));
       rec.push_back(stage_gemm(g3, allp, alls));
     }
+    // the descriptor arena wraps when full: the problem descriptors are
+    // staged again with every chunk so that they never predate a wrap
+    if (it0 > 0) dp = ar.put(probs, s);
     const GemmProb* gp = allp.empty() ? nullptr : ar.put(allp, s);
     const int* gs = alls.empty() ? nullptr : ar.put(alls, s);
     for (int q = 0; q < nit; ++q, ++it) {
@@ -751,6 +754,7 @@ void launch_qr_blocked(const std::vector<BqrProb>& probs, DescArena& ar, cudaStr
         for (const BqrProb& p : probs)
           if (j < p.s) fl += 2.0 * (p.m - j) * std::min(b, p.s - j) * std::min(b, p.s - j);
         ProfScope ps(K_QR, s, fl, 0);
+        if (j > 0) dp = ar.put(probs, s);   // the GEMM launches in between may have wrapped the arena
         bqr_panel_kernel<<<(unsigned)probs.size(), 512, smem_panel, s>>>(dp, j, b, J0, SB);
         post_launch();
       }

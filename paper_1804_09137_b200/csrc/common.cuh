@@ -216,6 +216,7 @@ class DescArena {
   void* put_bytes(const void* src, size_t bytes, cudaStream_t s);
   void reset() { off_ = 0; }
   size_t used() const { return off_; }
+  size_t capacity() const { return cap_; }
  private:
   char* h_ = nullptr; char* d_ = nullptr; size_t cap_ = 0, off_ = 0;
 };
@@ -227,9 +228,11 @@ void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStrea
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
 // multi-launch staging: build several batches on the host, upload once, launch
 struct GemmStaged { int poff = 0, soff = 0, moff = -1, n = 0, tot = 0, cfg = 0; double fl = 0, by = 0; bool vec = false; };
-GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls);
+GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls,
+                      int cfg = -1);   // cfg < 0: chosen from the batch
 void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s);
 void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, cudaStream_t s);
+void launch_trsm_panel(const std::vector<TrsmProb>& probs, DescArena& ar, cudaStream_t s);   // one shared L, blocked on DMMA
 void launch_potrf_block(double* A, int ld, int n, int r0, int bs, int tile, int* info,
                         double* logdiag, cudaStream_t s);
 // unpivoted blocked Householder QR (bqrcp.cu): R + reflectors in A (m x s),

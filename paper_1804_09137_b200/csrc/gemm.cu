@@ -284,32 +284,41 @@ void run_tiles(bool vec, int tot, const GemmProb* dp, const int* ds, const int* 
   else run_tiles_v<BM, BN, WM, WN, ST, KS, 1>(tot, dp, ds, dm, n, s);
 }
 
-// configuration of a batch: the larger tiles once the problems are large
-// enough to fill them (measured on the TLR batch shapes, tools/bench_gemm.cu)
+// tile configuration of one problem (measured on the TLR batch shapes,
+// tools/bench_gemm.cu): the larger tiles once the problem fills them
+static int prob_cfg(const GemmProb& p) {
+  if (p.m >= 256 && p.n >= 256 && p.k >= 64) return 2;
+  if (p.m >= 96 && p.n >= 96) return 1;
+  if (p.m <= 40 && p.n <= 40 && p.k >= 128) return 3;
+  if (p.m <= 40 && p.n >= 96) return 4;
+  return 0;
+}
+
+// configuration of a whole batch (one launch): the class that holds most of
+// the batch's flops, 64 x 64 tiles for mixed batches
 int pick_cfg(const std::vector<GemmProb>& probs) {
   static const int force = getenv("TLRB_GEMM_CFG") ? atoi(getenv("TLRB_GEMM_CFG")) : -1;
   if (force >= 0 && force < 5) return force;
-  double fl = 0, fl_big = 0, fl_huge = 0, fl_small = 0, fl_thin = 0;
+  double fl = 0, fc[5] = {0, 0, 0, 0, 0};
   for (const GemmProb& p : probs) {
     const double f = 2.0 * p.m * p.n * p.k;
     fl += f;
-    if (p.m >= 96 && p.n >= 96) fl_big += f;
-    if (p.m >= 256 && p.n >= 256 && p.k >= 64) fl_huge += f;
-    if (p.m <= 40 && p.n <= 40 && p.k >= 128) fl_small += f;
-    if (p.m <= 40 && p.n >= 96) fl_thin += f;
+    fc[prob_cfg(p)] += f;
+    if (prob_cfg(p) == 2) fc[1] += f;   // huge problems also fill the 64 x 128 tiles
   }
-  if (fl_huge >= 0.7 * fl) return 2;
-  if (fl_big >= 0.7 * fl) return 1;
-  if (fl_small >= 0.7 * fl) return 3;
-  if (fl_thin >= 0.7 * fl) return 4;
+  if (fc[2] >= 0.7 * fl) return 2;
+  if (fc[1] >= 0.7 * fl) return 1;
+  if (fc[3] >= 0.7 * fl) return 3;
+  if (fc[4] >= 0.7 * fl) return 4;
   return 0;
 }
 
 // host-side staging of one batched launch: appends the non-empty problems and
 // their tile prefix sums to (allp, alls); returns the launch record
-GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls) {
+GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls,
+                      int cfg) {
   GemmStaged g;
-  g.cfg = pick_cfg(probs);
+  g.cfg = cfg >= 0 ? cfg : pick_cfg(probs);
   const int bm = kCfg[g.cfg].bm, bn = kCfg[g.cfg].bn;
   g.poff = (int)allp.size();
   g.soff = (int)alls.size();
@@ -410,17 +419,58 @@ void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t
   }
 }
 
-void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
-  if (probs.empty()) return;
+static void launch_gemm_one(const std::vector<GemmProb>& probs, int cfg, DescArena& ar, cudaStream_t s) {
   std::vector<GemmProb> keep;
   std::vector<int> start;
   keep.reserve(probs.size());
   start.reserve(probs.size() + 1);
-  const GemmStaged g = stage_gemm(probs, keep, start);
+  const GemmStaged g = stage_gemm(probs, keep, start, cfg);
   if (g.tot == 0) return;
   const GemmProb* dp = ar.put(keep, s);
   const int* ds = ar.put(start, s);
   launch_gemm_staged(g, dp, ds, s);
+}
+
+// One call = one batch of independent problems.  A batch of mixed shapes
+// (the tile Cholesky's update batches hold exact 760^3 products next to
+// rank-20 ones) is split by tile configuration, one launch per class that
+// carries a real share of the work, so the large problems run on the
+// 128 x 128 tiles and the small ones do not pay for them; classes with little
+// work ride along with the dominant one.  TLRB_GEMM_SPLIT=0: one launch.
+void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  static const bool split = !(getenv("TLRB_GEMM_SPLIT") && atoi(getenv("TLRB_GEMM_SPLIT")) == 0) &&
+                            !getenv("TLRB_GEMM_CFG");
+  if (!split || probs.size() < 16) return launch_gemm_one(probs, -1, ar, s);
+  double fl = 0, fc[5] = {0, 0, 0, 0, 0};
+  int cnt[5] = {0, 0, 0, 0, 0};
+  for (const GemmProb& p : probs) {
+    if (p.m <= 0 || p.n <= 0) continue;
+    const double f = 2.0 * p.m * p.n * std::max(1, p.k);
+    const int c = prob_cfg(p);
+    fl += f;
+    fc[c] += f;
+    ++cnt[c];
+  }
+  int dom = 0, nsep = 0;
+  for (int c = 1; c < 5; ++c)
+    if (fc[c] > fc[dom]) dom = c;
+  bool sep[5];
+  for (int c = 0; c < 5; ++c) {
+    sep[c] = c == dom || (cnt[c] >= 8 && fc[c] >= 0.05 * fl);
+    nsep += sep[c];
+  }
+  if (nsep == 1) return launch_gemm_one(probs, -1, ar, s);
+  std::vector<GemmProb> grp[5];
+  for (const GemmProb& p : probs) {
+    if (p.m <= 0 || p.n <= 0) continue;
+    const int c = prob_cfg(p);
+    // a class without its own launch joins the 64 x 64 launch when there is one (any shape runs well enough there),
+    // else the dominant one
+    grp[sep[c] ? c : (sep[0] ? 0 : dom)].push_back(p);
+  }
+  for (int c = 0; c < 5; ++c)
+    if (!grp[c].empty()) launch_gemm_one(grp[c], c, ar, s);
 }
 
 }  // namespace tlrb

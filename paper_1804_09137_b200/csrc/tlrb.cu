@@ -82,6 +82,14 @@ double dense_frac() {
   return v;
 }
 
+// TLRB_FACTORED_OVER=0: updates whose stacked rank exceeds the dense limit
+// take the dense path (M formed, QRCP, exact storage decided on the QRCP
+// rank) instead of the factored one followed by a densify
+bool factored_over_limit() {
+  static const bool v = !(getenv("TLRB_FACTORED_OVER") && atoi(getenv("TLRB_FACTORED_OVER")) == 0);
+  return v;
+}
+
 // TLRB_DENSE_BY_QRCP=0: decide exact storage on the SVD truncation rank only
 // (the SVD of every capped tile runs); default: on the QRCP rank
 bool dense_by_qrcp() {
@@ -729,19 +737,35 @@ bool check_npd(tlrb_handle* h) {
 // ------------------------------------------------------ dense factorisation
 bool factor_dense(tlrb_handle* h) {
   const int t = h->t, nb = h->nb;
+  // look-ahead: POTRF(k+1) needs only step k's SYRK of D(k+1); it is
+  // launched first and the POTRF runs on the side stream beside the rest of
+  // the trailing update (linalg.py:82-103 order per tile is unchanged)
+  static const bool lookahead = !(getenv("TLRB_LOOKAHEAD") && atoi(getenv("TLRB_LOOKAHEAD")) == 0);
+  int ahead = -1;
   for (int k = 0; k < t; ++k) {
-    potrf(h, k);
+    if (ahead == k) TLRB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_potrf, 0));
+    else potrf(h, k);
     share_lkk(h, k);
     std::vector<TrsmProb> tp;
     for (int i = k + 1; i < t; ++i)
       if (h->own(i, k)) tp.push_back({h->Dk(k), nb, h->Ut(i, k), nb, h->sz[k], h->sz[i]});
-    launch_trsm(tp, false, h->ar, h->stream);
+    launch_trsm_panel(tp, h->ar, h->stream);
     bcast_panel(h, k, true);
+    if (lookahead && k + 1 < t && h->own(k + 1, k + 1)) {
+      const int j = k + 1;
+      launch_gemm({GemmProb{h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
+                            nb, 1, 0, 1, -1.0, 1.0}}, h->ar, h->stream);
+      TLRB_CUDA(cudaEventRecord(h->ev_syrk, h->stream));
+      TLRB_CUDA(cudaStreamWaitEvent(h->side, h->ev_syrk, 0));
+      potrf(h, j, h->side);
+      TLRB_CUDA(cudaEventRecord(h->ev_potrf, h->side));
+      ahead = j;
+    }
     std::vector<GemmProb> gp;
     const double nk = h->sz[k];
     for (int j = k + 1; j < t; ++j) {
-      // D_j -= L_jk L_jk^T = T_jk^T T_jk
-      if (h->own(j, j))
+      // D_j -= L_jk L_jk^T = T_jk^T T_jk  (j = k + 1 already went ahead of the look-ahead POTRF)
+      if (h->own(j, j) && ahead != j)
         gp.push_back({h->Ut(j, k), h->Ut(j, k), h->D(j), h->D(j), h->sz[j], h->sz[j], h->sz[k], nb, nb, nb,
                       nb, 1, 0, 1, -1.0, 1.0});
       h->work.add(nk * h->sz[j] * h->sz[j], 8.0 * (2.0 * nk * h->sz[j] + 2.0 * h->sz[j] * h->sz[j]));
@@ -790,7 +814,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
       if (r) tp.push_back({h->Dk(k), nb, h->Vt(i, k), nb, h->sz[k], r});
       if (r) h->work.add(nk * nk * r, 8.0 * (nk * nk / 2 + 2.0 * nk * r));
     }
-    launch_trsm(tp, false, h->ar, h->stream);
+    launch_trsm_panel(tp, h->ar, h->stream);
     // single GPU: the NPD flag is read with the next rank readback (no sync
     // here); a failed POTRF only lets this step's batch run on garbage.
     // Distributed: one all-reduce carries the flag and the panel's ranks.
@@ -924,7 +948,11 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         const bool fits = (size_t)(mi + mj) * K <= nb2s && 2 * (size_t)K * K <= nb2s &&
                           (size_t)4 * 128 * K <= nb2s &&
                           2 * ((size_t)128 * K + 16384) + (size_t)ki * kj <= nb2s;
-        return fits && K <= factored_frac(nb) * std::min(mi, mj) && K <= dense_rank_limit(h, mi, mj);
+        // under a storage cap both stacked parts are within the dense limit,
+        // so K <= 2 limit; a result above the limit is stored exactly after
+        // the recompression (densify below)
+        return fits && K <= factored_frac(nb) * std::min(mi, mj) &&
+               (factored_over_limit() || K <= dense_rank_limit(h, mi, mj));
       };
       // dense-path jobs first (slots 0..nd-1), factored ones after them
       std::vector<size_t> order;
@@ -1111,6 +1139,20 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           h->sync();
           fprintf(stderr, "[tlrb] apply-Q %zu factors %.2f ms\n", fp.size(), now_ms() - ta0);
         }
+        // storage rule (dense_frac): a recompressed tile whose rank exceeds
+        // the dense limit is kept as the exact product of its new factors,
+        // L_ij^T = V_new U_new^T, in a fresh dense slot (the factor slabs
+        // stay valid in the bump arena until the GEMM has read them)
+        std::vector<GemmProb> dens;
+        for (Job& J : jobs) {
+          if (!J.factored || J.out_rank <= dense_rank_limit(h, J.mu, J.nv)) continue;
+          const double* U = J.Ufin;
+          const double* V = J.Vfin;
+          h->ensure((size_t)J.ftile, nb, true);
+          dens.push_back({V, U, nullptr, h->uptr[J.ftile], J.nv, J.mu, J.out_rank, nb, nb, 0, nb, 0, 1, 0, 1.0, 0.0});
+          J.dense_out = true;
+        }
+        launch_gemm(dens, h->ar, h->stream);
       }
       for (size_t q = c0; q < c1; ++q) {
         const int i = upd[q].first, j = upd[q].second;
@@ -1535,7 +1577,12 @@ tlrb_handle* create_one(const double* xy, int64_t n, int nb, int max_rank, int d
     h->Q = Q;
     h->dworld = P * Q;
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    TLRB_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    {   // look-ahead POTRF stream: highest priority, so its few CTAs get the
+        // SM slots the main stream's large batches free up
+      int lo_prio = 0, hi_prio = 0;
+      TLRB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      TLRB_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi_prio));
+    }
     TLRB_CUDA(cudaStreamCreateWithFlags(&h->lane2, cudaStreamNonBlocking));
     TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
     TLRB_CUDA(cudaEventCreateWithFlags(&h->ev_f, cudaEventDisableTiming));
@@ -1581,7 +1628,11 @@ tlrb_handle* create_one(const double* xy, int64_t n, int nb, int max_rank, int d
     TLRB_CUDA(cudaMalloc(&h->d_scal, 4 * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_z, n * sizeof(double)));
     TLRB_CUDA(cudaMalloc(&h->d_w, (size_t)h->t * h->nb * sizeof(double)));
-    h->ar.init(64u << 20);
+    {   // launch-descriptor staging ring (TLRB_DESC_MB: smaller rings force the
+        // wrap path, tests/test_gpu_parity.py::test_descriptor_arena_wraps)
+      const int mb = getenv("TLRB_DESC_MB") ? std::max(1, atoi(getenv("TLRB_DESC_MB"))) : 64;
+      h->ar.init((size_t)mb << 20);
+    }
     // compression workspace: 8 nb^2 + 2 nb + 16 nb doubles per job slot
     h->slot_doubles = 8 * nb2 + 18 * (size_t)h->nb + 64;
     size_t freeb = 0, totb = 0;

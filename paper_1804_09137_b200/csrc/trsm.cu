@@ -7,6 +7,7 @@
 //     log-determinant (linalg.py:78-79).
 // The trailing rank-32 update of POTRF goes through the DMMA GEMM.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace tlrb {
 
@@ -146,6 +147,42 @@ void launch_trsm(const std::vector<TrsmProb>& probs, bool trans, DescArena& ar, 
     trsm_vbatch_kernel<false><<<tot, threads, smem, s>>>(dp, ds, (int)keep.size(), W);
   }
   post_launch();
+}
+
+// Panel solves of one Cholesky step: every problem applies the same L_kk
+// (n x n) to its own right-hand sides (dense tiles stored transposed, V
+// factors of low-rank tiles).  Blocked forward substitution over row blocks
+// of 128: the rows of the block are first updated with the solved rows above
+// by one batched DMMA GEMM (B_b -= L_b,0:b X_0:b, all problems in one launch),
+// then solved against the 128 x 128 diagonal block by the CUDA-core kernel,
+// which is left with n_b / n of the flops.  Small panels (n <= 256 or few
+// right-hand sides) keep the single-kernel path.  TLRB_TRSM_BLOCKED=0: always.
+void launch_trsm_panel(const std::vector<TrsmProb>& probs, DescArena& ar, cudaStream_t s) {
+  static const int IB = getenv("TLRB_TRSM_BLOCKED") ? atoi(getenv("TLRB_TRSM_BLOCKED")) : 128;
+  long rhs = 0;
+  int n = 0;
+  bool same = true;
+  for (const TrsmProb& p : probs) {
+    if (p.n <= 0 || p.nrhs <= 0) continue;
+    if (n == 0) n = p.n;
+    same &= p.n == n && p.L == probs[0].L;
+    rhs += p.nrhs;
+  }
+  if (IB <= 0 || !same || n <= 2 * IB || rhs < 256) return launch_trsm(probs, false, ar, s);
+  std::vector<TrsmProb> tb;
+  std::vector<GemmProb> gu;
+  for (int r0 = 0; r0 < n; r0 += IB) {
+    const int rb = std::min(IB, n - r0);
+    tb.clear(); gu.clear();
+    for (const TrsmProb& p : probs) {
+      if (p.n <= 0 || p.nrhs <= 0) continue;
+      if (r0 > 0)
+        gu.push_back({p.L + r0, p.B, p.B + r0, p.B + r0, rb, p.nrhs, r0, p.ldl, p.ldb, p.ldb, p.ldb, 0, 0, 0, -1.0, 1.0});
+      tb.push_back({p.L + (size_t)r0 * p.ldl + r0, p.ldl, p.B + r0, p.ldb, rb, p.nrhs});
+    }
+    launch_gemm(gu, ar, s);
+    launch_trsm(tb, false, ar, s);
+  }
 }
 
 // ------------------------------------------------------------------ POTRF

@@ -34,6 +34,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lead", type=int, nargs="*", default=[24, 48, 72])
     ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--offsets", type=int, nargs="*",
+                    default=[1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 526])
     a = ap.parse_args()
     full = tb.generate_locations(N, 0).coords
     p = tb.MaternParams(*THETA)
@@ -60,18 +62,68 @@ def main():
         h.close()
         del h
     Ls = np.array([r["L"] for r in runs], float)
-    Ts = np.array([r["s"] for r in runs])
-    coef, *_ = np.linalg.lstsq(np.stack([Ls ** 2, Ls ** 3], 1), Ts, rcond=None)
-    t1 = float(coef[0] * T_FULL ** 2 + coef[1] * T_FULL ** 3)
-    # stored memory of the full factor: per-offset storage of the largest
-    # block, extended to the full tile grid
+    tiles = Ls * (Ls + 1) / 2
+
+    def phase(k):
+        return np.array([r["phases_ms"][k] for r in runs]) / 1e3
+
+    # generation + compression: one unit of work per tile; the per-tile cost
+    # falls with the offset (smaller ranks), so the largest block's mean is
+    # an upper bound for the full grid
+    comp = phase("ms_generate")
+    per_tile = comp / tiles
+    n_tiles_full = T_FULL * (T_FULL + 1) / 2
+    comp_full = float(per_tile[-1] * n_tiles_full)
+    # factorisation: exact cubic through the measured blocks (upper estimate:
+    # the L^3 term assumes far updates cost what the measured ones do) and a
+    # band-limited quadratic least-squares fit (lower estimate)
+    fac = phase("ms_factor")
+    hi = lo = None
+    if len(runs) >= 3:
+        c3 = np.linalg.solve(np.stack([Ls[-3:], Ls[-3:] ** 2, Ls[-3:] ** 3], 1), fac[-3:])
+        hi = float(c3 @ [T_FULL, T_FULL ** 2, T_FULL ** 3])
+        c2, *_ = np.linalg.lstsq(np.stack([Ls, Ls ** 2], 1), fac, rcond=None)
+        lo = float(c2 @ [T_FULL, T_FULL ** 2])
+    sol = phase("ms_solve")
+    sol_full = float(sol[-1] * T_FULL / Ls[-1])   # two triangular sweeps over a band: ~ linear in L beyond the band
+
+    # initial rank per tile offset (tile (d, 0) of the full grid, compressed
+    # alone) -> storage of the assembled TLR matrix on the full tile grid
+    offs = [d for d in a.offsets if d < T_FULL]
+    prof = {}
+    for d in offs:
+        rows = np.ascontiguousarray(full[d * NB:(d + 1) * NB])
+        cols = np.ascontiguousarray(full[:NB])
+        blk = tb.matern_block(rows, cols, p)
+        prof[d] = int(tb.compress_tile(blk, ACC)[0].shape[1])
+    ds = sorted(prof)
+    rank_at = np.interp(np.arange(1, T_FULL), ds, [prof[d] for d in ds])
+    limit = min(0.25 * NB, CAP)
+    stored = float(NB * NB * 8 * T_FULL)   # diagonal tiles
+    dense_band = 0
+    for d in range(1, T_FULL):
+        r = rank_at[d - 1]
+        cnt = T_FULL - d
+        if r > limit:
+            stored += cnt * NB * NB * 8.0
+            dense_band = d
+        else:
+            stored += cnt * 2.0 * NB * (16 * np.ceil(r / 16)) * 8.0
     out = {"config": "C5", "n": N, "nb": NB, "acc": ACC, "max_rank": CAP, "tiles": T_FULL, "runs": runs,
-           "fit": {"a_L2": float(coef[0]), "b_L3": float(coef[1])},
-           "projected_s_per_eval_1gpu": t1,
-           "projected_s_per_eval_8gpu_ideal": t1 / 8,
-           "projected_20_eval_mle_8gpu_ideal_h": 20 * t1 / 8 / 3600,
-           "note": ("upper bound: T(L) = a L^2 + b L^3 fitted on leading blocks, extrapolated to L = 527; "
-                    "8-GPU figure assumes ideal strong scaling of the 2D block-cyclic schedule")}
+           "per_tile_compress_ms": [float(x) * 1e3 for x in per_tile],
+           "initial_rank_by_offset": prof,
+           "assembled_storage_gb": stored / 1e9, "exact_band_offsets": dense_band,
+           "projected_compress_s_1gpu": comp_full,
+           "projected_factor_s_1gpu": {"band_limited_fit": lo, "cubic_fit": hi},
+           "projected_solve_s_1gpu": sol_full,
+           "projected_s_per_eval_1gpu": [comp_full + (lo or 0) + sol_full, comp_full + (hi or 0) + sol_full],
+           "projected_s_per_eval_8gpu_ideal": [(comp_full + (lo or 0) + sol_full) / 8, (comp_full + (hi or 0) + sol_full) / 8],
+           "projected_20_eval_mle_8gpu_ideal_h": [20 * (comp_full + (lo or 0) + sol_full) / 8 / 3600,
+                                                  20 * (comp_full + (hi or 0) + sol_full) / 8 / 3600],
+           "note": ("leading L x L tile blocks of the full grid measured on one B200; compression extrapolated per "
+                    "tile, the factorisation between a band-limited fit a L + b L^2 (lower) and the exact cubic "
+                    "through the three largest blocks (upper); 8-GPU figures assume ideal strong scaling of the 2D "
+                    "block-cyclic schedule and that the factor (assembled_storage_gb plus fill) fits 8 x 180 GB")}
     print(json.dumps(out))
 
 
