@@ -227,7 +227,8 @@ void launch_gen_tiles(const std::vector<GenTile>& tiles, const Pts& pts, const M
 void launch_bessel(double nu, const double* x, double* out, int64_t n, cudaStream_t s);
 void launch_gemm(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s);
 // multi-launch staging: build several batches on the host, upload once, launch
-struct GemmStaged { int poff = 0, soff = 0, moff = -1, n = 0, tot = 0, cfg = 0; double fl = 0, by = 0; bool vec = false; };
+struct GemmStaged { int poff = 0, soff = 0, moff = -1, n = 0, tot = 0, cfg = 0; double fl = 0, by = 0; bool vec = false;
+                    int ta = -1, tb = -1; };   // one (ta, tb) per launch
 GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>& allp, std::vector<int>& alls,
                       int cfg = -1);   // cfg < 0: chosen from the batch
 void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, cudaStream_t s);

@@ -22,9 +22,13 @@
 
 namespace tlrb {
 
+#ifndef TLRB_GEMM_INTER
+#define TLRB_GEMM_INTER 1
+#endif
 constexpr int GBK = 16;        // K slab per pipeline stage
 constexpr int PADK = 4;        // k-contiguous smem rows: stride GBK + 4 (conflict-free fragments)
-constexpr int PADMN = 8;       // m/n-contiguous smem rows: stride BM/BN + 8
+constexpr int PADMN = 4;       // m/n-contiguous smem rows: stride BM/BN + 4 (= 4 mod 16: the four k rows of a
+                               // fragment land on distinct banks; + 8 gave 2-way conflicts, ncu r02f)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -57,17 +61,25 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // fragments; ST-stage cp.async pipeline of K slabs of 16.  Shared layouts
 // follow the operand's contiguous direction so that the asynchronous copies
 // are coalesced and the fragment reads hit distinct banks:
-//   op(A) = A   (m contiguous): As[k][m], stride BM + 8
+//   op(A) = A   (m contiguous): As[k][m], stride BM + 4
 //   op(A) = A^T (k contiguous): As[m][k], stride 16 + 4
 //   op(B) = B   (k contiguous): Bs[n][k], stride 16 + 4
-//   op(B) = B^T (n contiguous): Bs[k][n], stride BN + 8
-template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC>
+//   op(B) = B^T (n contiguous): Bs[k][n], stride BN + 4
+// The transposition flags are template parameters (a launch holds problems of
+// one (ta, tb) only): the shared-memory addresses of the fragment reads are
+// then immediates and the copy addresses advance by one add per slab.  ncu of
+// the runtime-flag version (r02f): 5.5 instructions issued per DMMA, most of
+// them SEL / IMAD / LEA address selection, FP64 tensor pipe 78% busy.
+template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC, bool TA, bool TB>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
     dgemm_tiles_kernel(const GemmProb* __restrict__ probs, const int* __restrict__ start,
                        const int* __restrict__ blk2p, int nprob) {
   constexpr int NT = (BM / WM) * (BN / WN) * KS * 32;
-  constexpr int AS = (BM + PADMN) * GBK > BM * (GBK + PADK) ? (BM + PADMN) * GBK : BM * (GBK + PADK);
-  constexpr int BS = (BN + PADMN) * GBK > BN * (GBK + PADK) ? (BN + PADMN) * GBK : BN * (GBK + PADK);
+  constexpr bool INTER = TLRB_GEMM_INTER;             // refill spread over the k-steps
+  constexpr int LSA = TA ? GBK + PADK : BM + PADMN;   // shared row strides
+  constexpr int LSB = TB ? BN + PADMN : GBK + PADK;
+  constexpr int AS = TA ? BM * LSA : GBK * LSA;       // doubles per stage
+  constexpr int BS = TB ? GBK * LSB : BN * LSB;
   constexpr int FM = WM / 8, FN = WN / 8;
   extern __shared__ double smem[];
   double* As = smem;              // ST x AS
@@ -91,7 +103,6 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
   const int m0 = (local % tm) * BM, n0 = (local / tm) * BN;
   if (P.lower_only && n0 >= m0 + BM) return;
   const int M = P.m, N = P.n, K = P.k, lda = P.lda, ldb = P.ldb;
-  const bool ta = P.ta, tb = P.tb;
   const double* __restrict__ A = P.A;
   const double* __restrict__ B = P.B;
 
@@ -106,55 +117,84 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
   // operand of the batch 16-byte aligned with an even leading dimension):
   // a thread moves pairs along the operand's contiguous direction with one
   // 16-byte cp.async (half the LDGSTS instructions, L1 bypassed).
+  //   A   (m contiguous): row pair a_r fixed, k = a_k + i NT / CM
+  //   A^T (k contiguous): k pair a_k fixed,   m = a_r + i NT / CK
+  //   B   (k contiguous): k pair b_k fixed,   n = b_c + i NT / CK
+  //   B^T (n contiguous): col pair b_c fixed, k = b_k + i NT / CN
   static_assert(NT % BM == 0 && NT % BN == 0 && NT % GBK == 0, "copy layout");
   constexpr int CM = BM / VEC, CN = BN / VEC, CK = GBK / VEC;   // copy positions along m / n / k
-  const int a_r = ta ? tid / CK : VEC * (tid % CM), a_k = ta ? VEC * (tid % CK) : tid / CM;
-  const int b_c = tb ? VEC * (tid % CN) : tid / CK, b_k = tb ? tid / CN : VEC * (tid % CK);
-  const double* a_base = ta ? A + (size_t)(m0 + a_r) * lda + a_k : A + (size_t)a_k * lda + m0 + a_r;
-  const double* b_base = tb ? B + (size_t)b_k * ldb + n0 + b_c : B + (size_t)(n0 + b_c) * ldb + b_k;
-  const int a_soff = ta ? a_r * (GBK + PADK) + a_k : a_k * (BM + PADMN) + a_r;
-  const int b_soff = tb ? b_k * (BN + PADMN) + b_c : b_c * (GBK + PADK) + b_k;
-
-  // one copy of VEC doubles; `left` = valid elements from this position on
-  // along the contiguous direction (<= 0: nothing), `ok` = the other index
-  auto cp = [&](double* sm, const double* g, const double* base, bool ok, int left) {
-    if constexpr (VEC == 1) cp_async8(sm, g, base, ok && left > 0);
-    else cp_async16(sm, g, base, ok ? 8 * max(0, min(2, left)) : 0);
+  constexpr int NA = TA ? BM * CK / NT : CM * GBK / NT;         // copies per thread and stage
+  constexpr int NB = TB ? CN * GBK / NT : BN * CK / NT;
+  constexpr int SA = TA ? NT / CK : NT / CM;                    // index step between a thread's copies
+  constexpr int SB = TB ? NT / CN : NT / CK;
+  const int a_r = TA ? tid / CK : VEC * (tid % CM), a_k = TA ? VEC * (tid % CK) : tid / CM;
+  const int b_c = TB ? VEC * (tid % CN) : tid / CK, b_k = TB ? tid / CN : VEC * (tid % CK);
+  const double* a_ptr = TA ? A + (size_t)(m0 + a_r) * lda + a_k : A + (size_t)a_k * lda + m0 + a_r;
+  const double* b_ptr = TB ? B + (size_t)b_k * ldb + n0 + b_c : B + (size_t)(n0 + b_c) * ldb + b_k;
+  const size_t a_gs = (size_t)SA * lda, b_gs = (size_t)SB * ldb;          // global step between copies
+  const size_t a_ks = TA ? GBK : (size_t)GBK * lda, b_ks = TB ? (size_t)GBK * ldb : GBK;   // per slab
+  const unsigned a_sm = (unsigned)__cvta_generic_to_shared(As + (TA ? a_r * LSA + a_k : a_k * LSA + a_r));
+  const unsigned b_sm = (unsigned)__cvta_generic_to_shared(Bs + (TB ? b_k * LSB + b_c : b_c * LSB + b_k));
+  // edge of the tile along m / n: bytes of a copy (0 = zero fill).  Along
+  // the contiguous direction the count is per thread, across it per copy.
+  auto edge = [](int left) { return 8 * max(0, min(VEC, left)); };
+  const int a_edge = TA ? 0 : edge(M - (m0 + a_r));
+  const int b_edge = TB ? edge(N - (n0 + b_c)) : 0;
+  unsigned a_rows = 0, b_cols = 0;   // bit i: copy i of the stage lies inside the matrix
+  if constexpr (TA) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) a_rows |= (unsigned)(m0 + a_r + i * SA < M) << i;
+  }
+  if constexpr (!TB) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) b_cols |= (unsigned)(n0 + b_c + i * SB < N) << i;
+  }
+  auto cp = [&](unsigned sa, const double* g, int bytes) {
+    // a zero-byte copy reads nothing (the address may lie past the matrix) and zero-fills
+    if constexpr (VEC == 1)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(bytes));
+    else
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(bytes));
   };
-  auto load_stage = [&](int st, int k0) {
-    double* as = As + st * AS + a_soff;
-    double* bs = Bs + st * BS + b_soff;
-    if (!ta) {   // A(m, k) at A[k lda + m]: rows a_r fixed, k = a_k + i NT / CM
-      const double* g = a_base + (size_t)k0 * lda;
-      const int left = M - (m0 + a_r);
+  // stage `st` <- slab at k0 (a_ptr / b_ptr already point at it).  `tail`:
+  // the slab crosses K (only the last one can): per-copy k tests
+  // (part q of np: every np-th copy; the main loop spreads the refill of a
+  // stage over its k-steps so that the copy instructions of one warp issue
+  // behind the DMMA burst of the other warp of its scheduler)
+  auto load_part = [&](int st, int k0, bool tail, int q, int np) {
+    const unsigned sa = a_sm + st * (AS * 8), sb = b_sm + st * (BS * 8);
 #pragma unroll
-      for (int i = 0; i < CM * GBK / NT; ++i)
-        cp(as + i * (NT / CM) * (BM + PADMN), g + (size_t)i * (NT / CM) * lda, A,
-           k0 + a_k + i * (NT / CM) < K, left);
-    } else {     // A^T: A(m, k) at A[m lda + k]: k = a_k fixed, m = a_r + i NT / CK
-      const double* g = a_base + k0;
-      const int left = K - (k0 + a_k);
-#pragma unroll
-      for (int i = 0; i < BM * CK / NT; ++i)
-        cp(as + i * (NT / CK) * (GBK + PADK), g + (size_t)i * (NT / CK) * lda, A,
-           m0 + a_r + i * (NT / CK) < M, left);
+    for (int i = 0; i < NA; ++i) {
+      if (i % np != q) continue;
+      int by;
+      if constexpr (TA) {
+        by = (a_rows >> i) & 1 ? VEC * 8 : 0;
+        if (tail) by = min(by, edge(K - (k0 + a_k)));
+      } else {
+        by = a_edge;
+        if (tail && k0 + a_k + i * SA >= K) by = 0;
+      }
+      cp(sa + i * (SA * LSA * 8), a_ptr + i * a_gs, by);
     }
-    if (!tb) {   // B(k, n) at B[n ldb + k]: k = b_k fixed, n = b_c + i NT / CK
-      const double* g = b_base + k0;
-      const int left = K - (k0 + b_k);
 #pragma unroll
-      for (int i = 0; i < BN * CK / NT; ++i)
-        cp(bs + i * (NT / CK) * (GBK + PADK), g + (size_t)i * (NT / CK) * ldb, B,
-           n0 + b_c + i * (NT / CK) < N, left);
-    } else {     // B^T: B(k, n) at B[k ldb + n]: n = b_c fixed, k = b_k + i NT / CN
-      const double* g = b_base + (size_t)k0 * ldb;
-      const int left = N - (n0 + b_c);
-#pragma unroll
-      for (int i = 0; i < CN * GBK / NT; ++i)
-        cp(bs + i * (NT / CN) * (BN + PADMN), g + (size_t)i * (NT / CN) * ldb, B,
-           k0 + b_k + i * (NT / CN) < K, left);
+    for (int i = 0; i < NB; ++i) {
+      if (i % np != q) continue;
+      int by;
+      if constexpr (TB) {
+        by = b_edge;
+        if (tail && k0 + b_k + i * SB >= K) by = 0;
+      } else {
+        by = (b_cols >> i) & 1 ? VEC * 8 : 0;
+        if (tail) by = min(by, edge(K - (k0 + b_k)));
+      }
+      cp(sb + i * (SB * LSB * 8), b_ptr + i * b_gs, by);
+    }
+    if (q == np - 1) {
+      a_ptr += a_ks;
+      b_ptr += b_ks;
     }
   };
+  auto load_stage = [&](int st, int k0, bool tail) { load_part(st, k0, tail, 0, 1); };
 
   double acc[FM][FN][2];
 #pragma unroll
@@ -162,43 +202,47 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
 #pragma unroll
     for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int nk = (K + GBK - 1) / GBK;
+  const int nk = (K + GBK - 1) / GBK, kfull = K / GBK;
 #pragma unroll
   for (int st = 0; st < ST - 1; ++st) {
-    if (st < nk) load_stage(st, st * GBK);
+    if (st < nk) load_stage(st, st * GBK, st >= kfull);
     cp_async_commit();
   }
+  // fragment reads: lane (fr, fk) takes row / column fr of an 8-wide
+  // fragment at k = fk of the k-step; all other offsets are immediates
   const int fr = lane >> 2, fk = lane & 3;
+  const double* af = As + (TA ? (wm + fr) * LSA + 4 * wk + fk : (4 * wk + fk) * LSA + wm + fr);
+  const double* bf = Bs + (TB ? (4 * wk + fk) * LSB + wn + fr : (wn + fr) * LSB + 4 * wk + fk);
+  constexpr int A_T = TA ? 8 * LSA : 8, A_Q = TA ? 4 * KS : 4 * KS * LSA;   // per fragment / per k-step
+  constexpr int B_T = TB ? 8 : 8 * LSB, B_Q = TB ? 4 * KS * LSB : 4 * KS;
+  int st_c = 0, st_l = (ST - 1) % ST;   // stage consumed / loaded in this iteration
   for (int kc = 0; kc < nk; ++kc) {
     cp_async_wait<ST - 2>();
     __syncthreads();
-    // refill the stage consumed at kc - 1 (everyone is past it)
-    {
-      const int kn = kc + ST - 1;
-      if (kn < nk) load_stage(kn % ST, kn * GBK);
-      cp_async_commit();
-    }
-    const double* as = As + (kc % ST) * AS;
-    const double* bs = Bs + (kc % ST) * BS;
+    // the stage consumed at kc - 1 (everyone is past it) is refilled in NQ
+    // parts, one after each k-step's DMMAs
+    const int kn = kc + ST - 1;
+    const bool more = kn < nk, tail = kn >= kfull;
+    const double* as = af + st_c * AS;
+    const double* bs = bf + st_c * BS;
+    constexpr int NQ = GBK / (4 * KS);
 #pragma unroll
-    for (int k4 = 4 * wk; k4 < GBK; k4 += 4 * KS) {
-      const int kr = k4 + fk;
+    for (int q = 0; q < NQ; ++q) {
       double a[FM], b[FN];
 #pragma unroll
-      for (int t = 0; t < FM; ++t) {
-        const int r = wm + t * 8 + fr;
-        a[t] = !ta ? as[kr * (BM + PADMN) + r] : as[r * (GBK + PADK) + kr];
-      }
+      for (int t = 0; t < FM; ++t) a[t] = as[q * A_Q + t * A_T];
 #pragma unroll
-      for (int t = 0; t < FN; ++t) {
-        const int c = wn + t * 8 + fr;
-        b[t] = !tb ? bs[c * (GBK + PADK) + kr] : bs[kr * (BN + PADMN) + c];
-      }
+      for (int t = 0; t < FN; ++t) b[t] = bs[q * B_Q + t * B_T];
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      if (INTER && more) load_part(st_l, kn * GBK, tail, q, NQ);
     }
+    if (!INTER && more) load_stage(st_l, kn * GBK, tail);
+    cp_async_commit();
+    st_c = st_c + 1 == ST ? 0 : st_c + 1;
+    st_l = st_l + 1 == ST ? 0 : st_l + 1;
   }
   cp_async_wait<0>();
   if constexpr (KS > 1) {   // sum the K slices' partial tiles through shared memory
@@ -261,27 +305,31 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
 struct GemmCfg { int bm, bn; };
 constexpr GemmCfg kCfg[5] = {{64, 64}, {64, 128}, {128, 128}, {32, 32}, {32, 128}};
 
-template <int BM, int BN, int WM, int WN, int ST>
-size_t tiles_smem() {
-  constexpr int AS = (BM + PADMN) * GBK > BM * (GBK + PADK) ? (BM + PADMN) * GBK : BM * (GBK + PADK);
-  constexpr int BS = (BN + PADMN) * GBK > BN * (GBK + PADK) ? (BN + PADMN) * GBK : BN * (GBK + PADK);
-  return (size_t)ST * (AS + BS) * sizeof(double);
-}
-
-template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC>
-void run_tiles_v(int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
-  auto kern = dgemm_tiles_kernel<BM, BN, WM, WN, ST, KS, VEC>;
+template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC, bool TA, bool TB>
+void run_tiles_t(int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
+  auto kern = dgemm_tiles_kernel<BM, BN, WM, WN, ST, KS, VEC, TA, TB>;
+  constexpr int AS = TA ? BM * (GBK + PADK) : GBK * (BM + PADMN);
+  constexpr int BS = TB ? GBK * (BN + PADMN) : BN * (GBK + PADK);
+  const size_t pipe = (size_t)ST * (AS + BS) * sizeof(double);
   const size_t red = (size_t)(KS - 1) * (BM / WM) * (BN / WN) * (WM / 8) * (WN / 8) * 2 * 32 * sizeof(double);
   const size_t epi = (size_t)(BM + 1) * BN * sizeof(double);
-  const size_t sm = std::max({tiles_smem<BM, BN, WM, WN, ST>(), red, epi});
+  const size_t sm = std::max({pipe, red, epi});
   allow_smem(kern, sm);
   kern<<<tot, (BM / WM) * (BN / WN) * KS * 32, sm, s>>>(dp, ds, dm, n);
 }
 
+template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC>
+void run_tiles_v(int ta, int tb, int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
+  if (ta && tb) run_tiles_t<BM, BN, WM, WN, ST, KS, VEC, true, true>(tot, dp, ds, dm, n, s);
+  else if (ta) run_tiles_t<BM, BN, WM, WN, ST, KS, VEC, true, false>(tot, dp, ds, dm, n, s);
+  else if (tb) run_tiles_t<BM, BN, WM, WN, ST, KS, VEC, false, true>(tot, dp, ds, dm, n, s);
+  else run_tiles_t<BM, BN, WM, WN, ST, KS, VEC, false, false>(tot, dp, ds, dm, n, s);
+}
+
 template <int BM, int BN, int WM, int WN, int ST, int KS = 1>
-void run_tiles(bool vec, int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
-  if (vec) run_tiles_v<BM, BN, WM, WN, ST, KS, 2>(tot, dp, ds, dm, n, s);
-  else run_tiles_v<BM, BN, WM, WN, ST, KS, 1>(tot, dp, ds, dm, n, s);
+void run_tiles(const GemmStaged& g, const GemmProb* dp, const int* ds, const int* dm, cudaStream_t s) {
+  if (g.vec) run_tiles_v<BM, BN, WM, WN, ST, KS, 2>(g.ta, g.tb, g.tot, dp, ds, dm, g.n, s);
+  else run_tiles_v<BM, BN, WM, WN, ST, KS, 1>(g.ta, g.tb, g.tot, dp, ds, dm, g.n, s);
 }
 
 // tile configuration of one problem (measured on the TLR batch shapes,
@@ -330,6 +378,9 @@ GemmStaged stage_gemm(const std::vector<GemmProb>& probs, std::vector<GemmProb>&
     // 16-byte copies need both operands 16-byte aligned with even leading dimensions
     if (((reinterpret_cast<uintptr_t>(p.A) | reinterpret_cast<uintptr_t>(p.B)) & 15) || ((p.lda | p.ldb) & 1))
       g.vec = false;
+    if (g.ta < 0) { g.ta = p.ta != 0; g.tb = p.tb != 0; }
+    if ((p.ta != 0) != (g.ta != 0) || (p.tb != 0) != (g.tb != 0))
+      throw CudaError(cudaErrorInvalidValue, "stage_gemm: mixed transposition flags in one launch", __FILE__, __LINE__);
     allp.push_back(p);
     alls.push_back(tot);
     tot += ((p.m + bm - 1) / bm) * ((p.n + bn - 1) / bn);
@@ -361,11 +412,11 @@ void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, 
   const int* st = ds + g.soff;
   const int* mp = g.moff >= 0 ? ds + g.moff : nullptr;
   switch (g.cfg) {
-    case 4: run_tiles<32, 128, 32, 64, 4, 2>(g.vec, g.tot, p, st, mp, g.n, s); break;
-    case 3: run_tiles<32, 32, 32, 32, 4, 4>(g.vec, g.tot, p, st, mp, g.n, s); break;
-    case 2: run_tiles<128, 128, 32, 64, 3>(g.vec, g.tot, p, st, mp, g.n, s); break;
-    case 1: run_tiles<64, 128, 32, 64, 3>(g.vec, g.tot, p, st, mp, g.n, s); break;
-    default: run_tiles<64, 64, 32, 32, 4>(g.vec, g.tot, p, st, mp, g.n, s); break;
+    case 4: run_tiles<32, 128, 32, 64, 4, 2>(g, p, st, mp, s); break;
+    case 3: run_tiles<32, 32, 32, 32, 4, 4>(g, p, st, mp, s); break;
+    case 2: run_tiles<128, 128, 32, 64, 3>(g, p, st, mp, s); break;
+    case 1: run_tiles<64, 128, 32, 64, 3>(g, p, st, mp, s); break;
+    default: run_tiles<64, 64, 32, 32, 4>(g, p, st, mp, s); break;
   }
   post_launch();
 }
@@ -437,7 +488,7 @@ static void launch_gemm_one(const std::vector<GemmProb>& probs, int cfg, DescAre
 // carries a real share of the work, so the large problems run on the
 // 128 x 128 tiles and the small ones do not pay for them; classes with little
 // work ride along with the dominant one.  TLRB_GEMM_SPLIT=0: one launch.
-void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
+static void launch_gemm_same_op(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
   if (probs.empty()) return;
   static const bool split = !(getenv("TLRB_GEMM_SPLIT") && atoi(getenv("TLRB_GEMM_SPLIT")) == 0) &&
                             !getenv("TLRB_GEMM_CFG");
@@ -445,7 +496,6 @@ void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStr
   double fl = 0, fc[5] = {0, 0, 0, 0, 0};
   int cnt[5] = {0, 0, 0, 0, 0};
   for (const GemmProb& p : probs) {
-    if (p.m <= 0 || p.n <= 0) continue;
     const double f = 2.0 * p.m * p.n * std::max(1, p.k);
     const int c = prob_cfg(p);
     fl += f;
@@ -463,7 +513,6 @@ void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStr
   if (nsep == 1) return launch_gemm_one(probs, -1, ar, s);
   std::vector<GemmProb> grp[5];
   for (const GemmProb& p : probs) {
-    if (p.m <= 0 || p.n <= 0) continue;
     const int c = prob_cfg(p);
     // a class without its own launch joins the 64 x 64 launch when there is one (any shape runs well enough there),
     // else the dominant one
@@ -471,6 +520,27 @@ void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStr
   }
   for (int c = 0; c < 5; ++c)
     if (!grp[c].empty()) launch_gemm_one(grp[c], c, ar, s);
+}
+
+// a launch holds one (ta, tb) combination (compile-time in the kernel): the
+// batch is cut by its transposition flags first (batches built by one code
+// path are uniform; the exact-tile updates of the TLR Cholesky mix three)
+void launch_gemm_impl(const std::vector<GemmProb>& probs, DescArena& ar, cudaStream_t s) {
+  if (probs.empty()) return;
+  bool uniform = true;
+  int first = -1;
+  for (const GemmProb& p : probs) {
+    if (p.m <= 0 || p.n <= 0) { uniform = false; continue; }   // dropped below
+    const int op = (p.ta != 0) * 2 + (p.tb != 0);
+    if (first < 0) first = op;
+    uniform &= op == first;
+  }
+  if (first < 0) return;
+  if (uniform) return launch_gemm_same_op(probs, ar, s);
+  std::vector<GemmProb> byop[4];
+  for (const GemmProb& p : probs)
+    if (p.m > 0 && p.n > 0) byop[(p.ta != 0) * 2 + (p.tb != 0)].push_back(p);
+  for (int o = 0; o < 4; ++o) launch_gemm_same_op(byop[o], ar, s);
 }
 
 }  // namespace tlrb
