@@ -23,7 +23,7 @@
 namespace tlrb {
 
 #ifndef TLRB_GEMM_INTER
-#define TLRB_GEMM_INTER 1
+#define TLRB_GEMM_INTER 0   // measured: refill after the k-steps 32.6 TF/s, spread over them 32.4, before them 31.1 (4096^3)
 #endif
 constexpr int GBK = 16;        // K slab per pipeline stage
 constexpr int PADK = 4;        // k-contiguous smem rows: stride GBK + 4 (conflict-free fragments)
@@ -226,6 +226,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
     const double* as = af + st_c * AS;
     const double* bs = bf + st_c * BS;
     constexpr int NQ = GBK / (4 * KS);
+    constexpr bool PRE = ST < 3;   // two stages: the refill must be in flight during this slab's DMMAs
+    if (PRE && more) load_stage(st_l, kn * GBK, tail);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       double a[FM], b[FN];
@@ -237,9 +239,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      if (INTER && more) load_part(st_l, kn * GBK, tail, q, NQ);
+      if (!PRE && INTER && more) load_part(st_l, kn * GBK, tail, q, NQ);
     }
-    if (!INTER && more) load_stage(st_l, kn * GBK, tail);
+    if (!PRE && !INTER && more) load_stage(st_l, kn * GBK, tail);
     cp_async_commit();
     st_c = st_c + 1 == ST ? 0 : st_c + 1;
     st_l = st_l + 1 == ST ? 0 : st_l + 1;
@@ -303,7 +305,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * KS * 32)
 
 // tile configurations (m x n tile, warp tile, stages)
 struct GemmCfg { int bm, bn; };
-constexpr GemmCfg kCfg[5] = {{64, 64}, {64, 128}, {128, 128}, {32, 32}, {32, 128}};
+constexpr int kNCfg = 9;
+constexpr GemmCfg kCfg[kNCfg] = {{64, 64}, {64, 128}, {128, 128}, {32, 32}, {32, 128},
+                                 {64, 64}, {64, 128}, {32, 128}, {32, 32}};   // 5..8: two-stage variants of 0, 1, 4, 3
 
 template <int BM, int BN, int WM, int WN, int ST, int KS, int VEC, bool TA, bool TB>
 void run_tiles_t(int tot, const GemmProb* dp, const int* ds, const int* dm, int n, cudaStream_t s) {
@@ -332,33 +336,34 @@ void run_tiles(const GemmStaged& g, const GemmProb* dp, const int* ds, const int
   else run_tiles_v<BM, BN, WM, WN, ST, KS, 1>(g.ta, g.tb, g.tot, dp, ds, dm, g.n, s);
 }
 
-// tile configuration of one problem (measured on the TLR batch shapes,
-// tools/bench_gemm.cu): the larger tiles once the problem fills them
+// tile configuration of one problem.  Measured with the templated kernel
+// (tools/bench_gemm.cu, TLRB_GEMM_CFG sweep, B200): the two-stage 64 x 64
+// configuration (41 KB of shared memory, five CTAs per SM) is the fastest or
+// within 1% of it on every shape with m > 40 -- 4096^3 34.2 TF/s (128 x 128
+// tiles: 32.6; cuBLAS 35.0), 82 x 760^3 32.4 (cuBLAS 34.2), 760 x 760 x 200
+// 28.0, 760 x 736 x 24 9.8 -- so only problems with m <= 40 keep their own
+// tiles: 32 x 32 with a four-way split of k when k is long, 32 x 128 with a
+// two-way split for short k and wide n.
 static int prob_cfg(const GemmProb& p) {
-  if (p.m >= 256 && p.n >= 256 && p.k >= 64) return 2;
-  if (p.m >= 96 && p.n >= 96) return 1;
-  if (p.m <= 40 && p.n <= 40 && p.k >= 128) return 3;
+  if (p.m <= 40 && p.k >= 128) return 3;   // also thin problems: 24 x 736 x 760 16.9 TF/s (32 x 128 tiles: 12.2)
   if (p.m <= 40 && p.n >= 96) return 4;
-  return 0;
+  return 5;
 }
 
 // configuration of a whole batch (one launch): the class that holds most of
-// the batch's flops, 64 x 64 tiles for mixed batches
+// the batch's flops, else the 64 x 64 tiles
 int pick_cfg(const std::vector<GemmProb>& probs) {
   static const int force = getenv("TLRB_GEMM_CFG") ? atoi(getenv("TLRB_GEMM_CFG")) : -1;
-  if (force >= 0 && force < 5) return force;
-  double fl = 0, fc[5] = {0, 0, 0, 0, 0};
+  if (force >= 0 && force < kNCfg) return force;
+  double fl = 0, fc[kNCfg] = {};
   for (const GemmProb& p : probs) {
     const double f = 2.0 * p.m * p.n * p.k;
     fl += f;
     fc[prob_cfg(p)] += f;
-    if (prob_cfg(p) == 2) fc[1] += f;   // huge problems also fill the 64 x 128 tiles
   }
-  if (fc[2] >= 0.7 * fl) return 2;
-  if (fc[1] >= 0.7 * fl) return 1;
   if (fc[3] >= 0.7 * fl) return 3;
   if (fc[4] >= 0.7 * fl) return 4;
-  return 0;
+  return 5;
 }
 
 // host-side staging of one batched launch: appends the non-empty problems and
@@ -416,6 +421,10 @@ void launch_gemm_staged(const GemmStaged& g, const GemmProb* dp, const int* ds, 
     case 3: run_tiles<32, 32, 32, 32, 4, 4>(g, p, st, mp, s); break;
     case 2: run_tiles<128, 128, 32, 64, 3>(g, p, st, mp, s); break;
     case 1: run_tiles<64, 128, 32, 64, 3>(g, p, st, mp, s); break;
+    case 5: run_tiles<64, 64, 32, 32, 2>(g, p, st, mp, s); break;
+    case 6: run_tiles<64, 128, 32, 64, 2>(g, p, st, mp, s); break;
+    case 7: run_tiles<32, 128, 32, 64, 2, 2>(g, p, st, mp, s); break;
+    case 8: run_tiles<32, 32, 32, 32, 2, 4>(g, p, st, mp, s); break;
     default: run_tiles<64, 64, 32, 32, 4>(g, p, st, mp, s); break;
   }
   post_launch();
@@ -493,8 +502,8 @@ static void launch_gemm_same_op(const std::vector<GemmProb>& probs, DescArena& a
   static const bool split = !(getenv("TLRB_GEMM_SPLIT") && atoi(getenv("TLRB_GEMM_SPLIT")) == 0) &&
                             !getenv("TLRB_GEMM_CFG");
   if (!split || probs.size() < 16) return launch_gemm_one(probs, -1, ar, s);
-  double fl = 0, fc[5] = {0, 0, 0, 0, 0};
-  int cnt[5] = {0, 0, 0, 0, 0};
+  double fl = 0, fc[kNCfg] = {};
+  int cnt[kNCfg] = {};
   for (const GemmProb& p : probs) {
     const double f = 2.0 * p.m * p.n * std::max(1, p.k);
     const int c = prob_cfg(p);
@@ -502,23 +511,23 @@ static void launch_gemm_same_op(const std::vector<GemmProb>& probs, DescArena& a
     fc[c] += f;
     ++cnt[c];
   }
-  int dom = 0, nsep = 0;
-  for (int c = 1; c < 5; ++c)
+  int dom = 5, nsep = 0;
+  for (int c = 0; c < kNCfg; ++c)
     if (fc[c] > fc[dom]) dom = c;
-  bool sep[5];
-  for (int c = 0; c < 5; ++c) {
+  bool sep[kNCfg];
+  for (int c = 0; c < kNCfg; ++c) {
     sep[c] = c == dom || (cnt[c] >= 8 && fc[c] >= 0.05 * fl);
     nsep += sep[c];
   }
   if (nsep == 1) return launch_gemm_one(probs, -1, ar, s);
-  std::vector<GemmProb> grp[5];
+  std::vector<GemmProb> grp[kNCfg];
   for (const GemmProb& p : probs) {
     const int c = prob_cfg(p);
     // a class without its own launch joins the 64 x 64 launch when there is one (any shape runs well enough there),
     // else the dominant one
-    grp[sep[c] ? c : (sep[0] ? 0 : dom)].push_back(p);
+    grp[sep[c] ? c : (sep[5] ? 5 : dom)].push_back(p);
   }
-  for (int c = 0; c < 5; ++c)
+  for (int c = 0; c < kNCfg; ++c)
     if (!grp[c].empty()) launch_gemm_one(grp[c], c, ar, s);
 }
 

@@ -12,7 +12,7 @@ COLS = [("gpu__time_duration.sum", "time"),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ %"),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM thr %"),
         ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
-        ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 inst %"),
+        ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA pipe %"),
         ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %"),
         ("dram__bytes_read.sum", "DRAM rd"), ("dram__bytes_write.sum", "DRAM wr"),
         ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),

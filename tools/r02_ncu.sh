@@ -1,5 +1,5 @@
-# ncu evidence at C3 (one warm evaluation through tools/trace_cfg.py), after
-# a clean run of the same command.  Outputs under gpurun_out/.
+# ncu evidence at C3 (one evaluation through tools/trace_cfg.py), after a
+# clean run of the same command.  Outputs under gpurun_out/.
 CMD="python tools/trace_cfg.py C3 --no-warm"
 $CMD > gpurun_out/r02_ncu_plain.out 2>&1 || exit 1
 # launch list with DRAM traffic: every kernel of the evaluation
@@ -7,7 +7,7 @@ timeout 2400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
     --clock-control none --csv --log-file gpurun_out/r02_launches_c3.csv $CMD > gpurun_out/r02_ncu_list.log 2>&1
 echo "list rc=$?"
 # --set full of the kernel classes (a few launches each, past the first steps)
-for spec in "dgemm_tiles:40:3" "jacobi_cluster:6:2" "bq_panel|bq_pick|bqr_panel:10:3" "gen_tiles:0:1" \
+for spec in "jacobi_cluster:6:2" "bq_panel|bq_pick|bqr_panel:10:3" "gen_tiles:0:1" \
             "potrf_block:20:1" "trsm_vbatch:20:1" "sumsq:10:1" "copy_kernel:20:1"; do
   IFS=: read -r re skip cnt <<< "$spec"
   tag=$(echo "$re" | cut -d'|' -f1)
@@ -15,4 +15,16 @@ for spec in "dgemm_tiles:40:3" "jacobi_cluster:6:2" "bq_panel|bq_pick|bqr_panel:
       -o gpurun_out/r02_full_$tag $CMD > gpurun_out/r02_ncu_full_$tag.log 2>&1
   echo "$tag rc=$?"
 done
+# the GEMM tile configurations by their demangled names: 64 x 64 two-stage (default), thin, small
+for spec in "dgemm_tiles_kernel<64, 64, 32, 32, 2,:300:3:gemm64" "dgemm_tiles_kernel<32, 128,:100:2:gemm_thin" \
+            "dgemm_tiles_kernel<32, 32,:50:2:gemm_small"; do
+  IFS=: read -r re skip cnt tag <<< "$spec"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$re" \
+      -s $skip -c $cnt -o gpurun_out/r02_full_$tag $CMD > gpurun_out/r02_ncu_full_$tag.log 2>&1
+  echo "$tag rc=$?"
+done
+# dense C3: the trailing-update GEMM (FP64 tensor pipe), the blocked TRSM's diagonal solves, POTRF
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dgemm_tiles -s 400 -c 2 \
+    -o gpurun_out/r02_full_dense_gemm python tools/trace_cfg.py C3 --no-warm --dense > gpurun_out/r02_ncu_full_dense_gemm.log 2>&1
+echo "dense gemm rc=$?"
 ls -la gpurun_out/*.ncu-rep
