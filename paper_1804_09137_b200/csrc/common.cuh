@@ -146,7 +146,8 @@ struct JacobiProb {        // one-sided Jacobi on the columns of X (m x s)
 
 // ----------------------------------------------------------- small helpers
 struct SumsqProb { const double* A; int ld, m, n; double* out; };
-// dst(r, c) = scale * (transpose ? src(c, r) : src(r, c)); tri: zero where r < c;
+// dst(r, c) = scale * (transpose ? src(c, r) : src(r, c)); tri = 1: zero where r < c;
+// tri = 2: dst(r, c) += scale * src (accumulate); src == nullptr: zero fill;
 // rowperm: dst row rowperm[r] receives row r
 // srccol (transpose mode): dst row r reads source column srccol[r]
 struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale;
@@ -252,6 +253,10 @@ void launch_qrcp(const std::vector<QrcpProb>& probs, std::vector<char>& gathered
 void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_jacobi(const std::vector<JacobiProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sumsq(const std::vector<SumsqProb>& probs, DescArena& ar, cudaStream_t s);
+// columns of A (m x n, ld) scaled to unit norm in place; their norms go to the diagonal diag[c (ldd + 1)]
+// (A == nullptr: the diagonal is set to one)
+struct ColNormProb { double* A; int ld, m, n; double* diag; int ldd; };
+void launch_colnorm(const std::vector<ColNormProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t s);
 void launch_sum_log(const double* logdiag, int n, double* out, cudaStream_t s);
 void launch_dot(const double* x, int n, double* out, cudaStream_t s);

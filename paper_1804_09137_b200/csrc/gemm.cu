@@ -486,9 +486,13 @@ static void launch_gemm_one(const std::vector<GemmProb>& probs, int cfg, DescAre
   start.reserve(probs.size() + 1);
   const GemmStaged g = stage_gemm(probs, keep, start, cfg);
   if (g.tot == 0) return;
-  const GemmProb* dp = ar.put(keep, s);
-  const int* ds = ar.put(start, s);
-  launch_gemm_staged(g, dp, ds, s);
+  // descriptors and tile prefix sums in one upload
+  const size_t pb = keep.size() * sizeof(GemmProb), sb = start.size() * sizeof(int);
+  std::vector<char> buf(pb + sb);
+  memcpy(buf.data(), keep.data(), pb);
+  memcpy(buf.data() + pb, start.data(), sb);
+  const char* d = static_cast<const char*>(ar.put_bytes(buf.data(), buf.size(), s));
+  launch_gemm_staged(g, reinterpret_cast<const GemmProb*>(d), reinterpret_cast<const int*>(d + pb), s);
 }
 
 // One call = one batch of independent problems.  A batch of mixed shapes

@@ -229,9 +229,10 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyProb* __restrict__ 
     double v = !P.src ? 0.0   // no source: zero fill
                : P.transpose ? P.src[(size_t)(P.srccol ? P.srccol[r] : r) * P.lds + c]
                              : P.src[(size_t)c * P.lds + r];
-    if (P.tri && r < c) v = 0.0;
+    if (P.tri == 1 && r < c) v = 0.0;
     const int rd = P.rowperm ? P.rowperm[r] : r;
-    P.dst[(size_t)c * P.ldd + rd] = P.scale * v;
+    double* d = P.dst + (size_t)c * P.ldd + rd;
+    *d = P.tri == 2 ? *d + P.scale * v : P.scale * v;
   }
 }
 
@@ -250,6 +251,43 @@ void launch_copy(const std::vector<CopyProb>& probs, DescArena& ar, cudaStream_t
   for (const CopyProb& p : keep) by += 16.0 * p.m * p.n;
   ProfScope ps(K_COPY, s, 0, by);
   copy_kernel<<<(unsigned)(keep.size() * chunks), 256, 0, s>>>(dp, chunks);
+  post_launch();
+}
+
+// ------------------------------------------- column normalisation (factored
+// recompression: the kept factor U_ij = Q D has orthogonal columns; Q goes
+// back in place and D onto the diagonal of the stacked R factor)
+__global__ void __launch_bounds__(256) colnorm_kernel(const ColNormProb* __restrict__ probs) {
+  const ColNormProb P = probs[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < P.n; c += nw) {
+    if (!P.A) {
+      if (lane == 0) P.diag[(size_t)c * (P.ldd + 1)] = 1.0;
+      continue;
+    }
+    double* col = P.A + (size_t)c * P.ld;
+    double a = 0.0;
+    for (int r = lane; r < P.m; r += 32) a = fma(col[r], col[r], a);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const double nrm = sqrt(a), inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int r = lane; r < P.m; r += 32) col[r] *= inv;
+    if (lane == 0) P.diag[(size_t)c * (P.ldd + 1)] = nrm;
+  }
+}
+
+void launch_colnorm(const std::vector<ColNormProb>& probs, DescArena& ar, cudaStream_t s) {
+  std::vector<ColNormProb> keep;
+  double by = 0;
+  for (const ColNormProb& p : probs)
+    if (p.n > 0) {
+      keep.push_back(p);
+      by += p.A ? 24.0 * p.m * p.n : 8.0 * p.n;
+    }
+  if (keep.empty()) return;
+  const ColNormProb* dp = ar.put(keep, s);
+  ProfScope ps(K_COPY, s, 0, by);
+  colnorm_kernel<<<(unsigned)keep.size(), 256, 0, s>>>(dp);
   post_launch();
 }
 
