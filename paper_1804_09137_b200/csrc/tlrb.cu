@@ -320,10 +320,10 @@ struct Job {
   BqrProb qu{}, qv{};
   int mu = 0, nv = 0;
   double* Ufin = nullptr; double* Vfin = nullptr;
-  // orthogonal-part shortcut of the factored path: the kept factors' k1
-  // columns are not refactored (Q1u = U_ij D^-1, Q1v = V_ij in the slot)
+  // orthogonal-part shortcut of the factored path (V side): the kept
+  // factor's k1 columns are not refactored (Q1v = V_ij in the slot)
   int k1 = 0;
-  double* Q1u = nullptr; double* Q1v = nullptr;
+  double* Q1v = nullptr;
   long tile = -1;     // destination tile (outputs allocated once the rank is known)
   long ftile = -1;    // factored path: destination tile of Qu u_core / Qv v_core
 };
@@ -1024,48 +1024,36 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           fsq.push_back({nullptr, 0, 0, 0, S + 3});
           fsq.push_back({Vs, mj, mj, K, S + 4});
           fsq.push_back({nullptr, 0, 0, 0, S + 5});
+          // U side: Householder QR of all K stacked columns, R^T (lower) into E
+          fq.push_back({Us, mi, mi, K, Vu, Tu, Wu});
+          fr.push_back({Us, mi, J.E, K, K, K, 1, 1.0, 1, nullptr});
           if (factored_ortho() && kij > 0) {
-            // The kept factors are already orthogonal: U_ij = Q1 D (columns
-            // orthogonal, D their norms) and V_ij orthonormal (outputs of the
-            // previous SVD), so the QR of the stacked factors is
-            //   [Q1 D, Y] = [Q1, Q2] [[D, Q1^T Y], [0, R2]],  Q2 R2 = (I - Q1 Q1^T) Y,
+            // V side: the kept factor V_ij is orthonormal to roundoff (the
+            // normalised Jacobi columns of the previous SVD, or Q times
+            // them), so the QR of the stacked factor is
+            //   [V1, W] = [V1, Q2] [[I, V1^T W], [0, R2]],  Q2 R2 = (I - V1 V1^T) W,
             // with the projection done twice by GEMMs (CGS2) and only the ku
-            // update columns refactored by Householder panels: the panel work
-            // falls from K to ku columns.  The identity holds to roundoff
-            // whatever the orthogonality of Q1 (1e-9 on its smallest columns).
-            double* Yp = Us + (size_t)mi * kij;
+            // update columns refactored by Householder panels.  (The U side
+            // cannot take the shortcut: U_ij = M V_k carries the QRCP
+            // residual, 1e-2 acc ||M||, so its smallest columns are
+            // orthogonal to 1e-2 only; treating them as orthogonal moved
+            // the C4p TLR(1e-9) likelihood by 2e-7, cond 4e8.)
             double* Wp = Vs + (size_t)mj * kij;
-            Vv = J.Q + (size_t)mi * ku;
-            double* C2u = J.Q + (size_t)(mi + mj) * ku;   // ku x kij each
-            double* C2v = C2u + (size_t)ku * kij;
-            double* C1u = J.E + kij;                      // block (kij.., 0..kij) of Ru^T, ld K
-            double* C1v = J.Bt + kij;
-            fz.push_back({nullptr, 0, J.E, K, K, K, 0, 1.0, 0, nullptr});
+            double* C2v = Vv + (size_t)mj * ku;   // ku x kij
+            double* C1v = J.Bt + kij;             // block (kij.., 0..kij) of Rv^T, ld K
             fz.push_back({nullptr, 0, J.Bt, K, K, K, 0, 1.0, 0, nullptr});
-            fcn.push_back({Us, mi, mi, kij, J.E, K});
             fcn.push_back({nullptr, 0, 0, kij, J.Bt, K});
-            oa1.push_back({Yp, Us, nullptr, C1u, ku, kij, mi, mi, mi, 0, K, 1, 0, 0, 1.0, 0.0});
             oa1.push_back({Wp, Vs, nullptr, C1v, ku, kij, mj, mj, mj, 0, K, 1, 0, 0, 1.0, 0.0});
-            ob1.push_back({Us, C1u, Yp, Yp, mi, ku, kij, mi, K, mi, mi, 0, 1, 0, -1.0, 1.0});
             ob1.push_back({Vs, C1v, Wp, Wp, mj, ku, kij, mj, K, mj, mj, 0, 1, 0, -1.0, 1.0});
-            oa2.push_back({Yp, Us, nullptr, C2u, ku, kij, mi, mi, mi, 0, ku, 1, 0, 0, 1.0, 0.0});
             oa2.push_back({Wp, Vs, nullptr, C2v, ku, kij, mj, mj, mj, 0, ku, 1, 0, 0, 1.0, 0.0});
-            ob2.push_back({Us, C2u, Yp, Yp, mi, ku, kij, mi, ku, mi, mi, 0, 1, 0, -1.0, 1.0});
             ob2.push_back({Vs, C2v, Wp, Wp, mj, ku, kij, mj, ku, mj, mj, 0, 1, 0, -1.0, 1.0});
-            facc.push_back({C2u, ku, C1u, K, ku, kij, 0, 1.0, 2, nullptr});
             facc.push_back({C2v, ku, C1v, K, ku, kij, 0, 1.0, 2, nullptr});
-            fq.push_back({Yp, mi, mi, ku, Vu, Tu, Wu});
             fq.push_back({Wp, mj, mj, ku, Vv, Tv, Wv});
-            fr.push_back({Yp, mi, J.E + (size_t)kij * K + kij, K, ku, ku, 1, 1.0, 1, nullptr});
             fr.push_back({Wp, mj, J.Bt + (size_t)kij * K + kij, K, ku, ku, 1, 1.0, 1, nullptr});
             J.k1 = kij;
-            J.Q1u = Us;
             J.Q1v = Vs;
           } else {
-            fq.push_back({Us, mi, mi, K, Vu, Tu, Wu});
             fq.push_back({Vs, mj, mj, K, Vv, Tv, Wv});
-            // R^T (lower) of both, then core = Ru Rv^T = (Ru^T)^T (Rv^T)
-            fr.push_back({Us, mi, J.E, K, K, K, 1, 1.0, 1, nullptr});
             fr.push_back({Vs, mj, J.Bt, K, K, K, 1, 1.0, 1, nullptr});
           }
           fcore.push_back({J.E, J.Bt, nullptr, J.M, K, K, K, K, K, K, K, 1, 0, 0, 1.0, 0.0});
@@ -1174,7 +1162,7 @@ bool factor_tlr(tlrb_handle* h, double acc) {
         std::vector<double*> fc;
         std::vector<int> fld, fk;
         std::vector<CopyProb> fin;
-        std::vector<GemmProb> fq1;   // U_new += Q1u u_core[0:k1], V_new += Q1v v_core[0:k1]
+        std::vector<GemmProb> fq1;   // V_new += V1 v_core[0:k1]
         for (Job& J : jobs) {
           if (!J.factored || !J.out_rank) continue;
           const int kk = J.out_rank;
@@ -1182,17 +1170,22 @@ bool factor_tlr(tlrb_handle* h, double acc) {
           J.Ufin = h->uptr[J.ftile];
           J.Vfin = h->vptr[J.ftile];
           // [core factor; 0] (K x kk on top of mu - K zero rows), then Q applied in place
-          // (orthogonal-part shortcut: rows k1.. of the core factors belong to Q2; Q1's share is added below)
-          const int q2 = J.m - J.k1;
-          fin.push_back({J.Uout + J.k1, J.ldu, J.Ufin, nb, q2, kk, 0, 1.0, 0, nullptr});
+          // (orthogonal-part shortcut on the V side: rows k1.. of the core
+          // factor belong to Q2; V1's share is added after the Q application)
+          const int q2 = J.n - J.k1;
+          fin.push_back({J.Uout, J.ldu, J.Ufin, nb, J.m, kk, 0, 1.0, 0, nullptr});
           fin.push_back({J.Vout + J.k1, J.ldv, J.Vfin, nb, q2, kk, 0, 1.0, 0, nullptr});
           // zero rows below the core factor (batched zero fill: one launch
           // for the whole batch instead of two memsets per job)
-          fin.push_back({nullptr, 0, J.Ufin + q2, nb, J.mu - q2, kk, 0, 1.0, 0, nullptr});
+          fin.push_back({nullptr, 0, J.Ufin + J.m, nb, J.mu - J.m, kk, 0, 1.0, 0, nullptr});
           fin.push_back({nullptr, 0, J.Vfin + q2, nb, J.nv - q2, kk, 0, 1.0, 0, nullptr});
           if (J.k1) {
-            fq1.push_back({J.Q1u, J.Uout, J.Ufin, J.Ufin, J.mu, kk, J.k1, J.mu, J.ldu, nb, nb, 0, 0, 0, 1.0, 1.0});
-            fq1.push_back({J.Q1v, J.Vout, J.Vfin, J.Vfin, J.nv, kk, J.k1, J.nv, J.ldv, nb, nb, 0, 0, 0, 1.0, 1.0});
+            // the Q application below uses the slot's F region (where the core
+            // factors live) as scratch: V1's rows of the core factor are
+            // saved in the M region first (the core is consumed by now)
+            double* sv = J.M;
+            fin.push_back({J.Vout, J.ldv, sv, J.k1, J.k1, kk, 0, 1.0, 0, nullptr});
+            fq1.push_back({J.Q1v, sv, J.Vfin, J.Vfin, J.nv, kk, J.k1, J.nv, J.k1, nb, nb, 0, 0, 0, 1.0, 1.0});
           }
           fp.push_back(J.qu); fc.push_back(J.Ufin); fld.push_back(nb); fk.push_back(kk);
           fp.push_back(J.qv); fc.push_back(J.Vfin); fld.push_back(nb); fk.push_back(kk);

@@ -16,15 +16,15 @@ for spec in "jacobi_cluster:6:2" "bq_panel|bq_pick|bqr_panel:10:3" "gen_tiles:0:
   echo "$tag rc=$?"
 done
 # the GEMM tile configurations by their demangled names: 64 x 64 two-stage (default), thin, small
-for spec in "dgemm_tiles_kernel<64, 64, 32, 32, 2,:300:3:gemm64" "dgemm_tiles_kernel<32, 128,:100:2:gemm_thin" \
-            "dgemm_tiles_kernel<32, 32,:50:2:gemm_small"; do
+for spec in "dgemm_tiles_kernel<.int.64, .int.64, .int.32, .int.32, .int.2,:300:3:gemm64" \
+            "dgemm_tiles_kernel<.int.32, .int.32,:50:2:gemm_small"; do
   IFS=: read -r re skip cnt tag <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$re" \
       -s $skip -c $cnt -o gpurun_out/r02_full_$tag $CMD > gpurun_out/r02_ncu_full_$tag.log 2>&1
   echo "$tag rc=$?"
 done
 # dense C3: the trailing-update GEMM (FP64 tensor pipe), the blocked TRSM's diagonal solves, POTRF
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dgemm_tiles -s 400 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dgemm_tiles -s 60 -c 6 \
     -o gpurun_out/r02_full_dense_gemm python tools/trace_cfg.py C3 --no-warm --dense > gpurun_out/r02_ncu_full_dense_gemm.log 2>&1
 echo "dense gemm rc=$?"
 ls -la gpurun_out/*.ncu-rep
