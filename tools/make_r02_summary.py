@@ -26,10 +26,12 @@ print("## Launch list of one evaluation\n")
 print("`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` on "
       "`python tools/trace_cfg.py C3 --no-warm` (`tools/r02_ncu.sh`; raw list: `profiles/r02_launches_c3.csv.gz`). "
       "Launches are serialised and cold-cache under ncu: compare shares, not absolutes.\n")
-print(run("tools/ncu_list_summary.py", str(G / "r02_launches_c3.csv"), "--md"))
+_csv = G / "r02_launches_c3.csv.gz"
+print(run("tools/ncu_list_summary.py", str(_csv if _csv.exists() else G / "r02_launches_c3.csv"), "--md"))
 print("\n## Counters per kernel class (`ncu --set full`, launches past the first steps)\n")
+_cnt = G / "r02_counters.md"
 reps = sorted(glob.glob(str(G / "r02_full_*.ncu-rep")))
-print(run("tools/ncu_rep_table.py", *reps))
+print(_cnt.read_text() if _cnt.exists() else run("tools/ncu_rep_table.py", *reps))
 print("\nGEMM microbenchmark (`tools/bench_gemm`, ours vs cuBLAS on the TLR shapes): `profiles/r02_gemm_bench.txt`.\n")
 notes = ROOT / "profiles" / "r02_summary_notes.md"
 if notes.exists():

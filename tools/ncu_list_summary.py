@@ -6,7 +6,9 @@ import csv
 import sys
 from collections import defaultdict
 
-lines = open(sys.argv[1]).read().splitlines()
+import gzip
+_p = sys.argv[1]
+lines = (gzip.open(_p, "rt") if _p.endswith(".gz") else open(_p)).read().splitlines()
 start = [i for i, l in enumerate(lines) if l.startswith('"ID"')][0]
 rows = list(csv.reader(lines[start:]))
 ix = {h: i for i, h in enumerate(rows[0])}
