@@ -1,4 +1,5 @@
 # session-5 call N: MLE protocol at C3, C5 leading blocks and C4 TLR(1e-9) with the final code
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 mkdir -p gpurun_out
 timeout 900 python tools/run_mle.py C3 > gpurun_out/r02_mle_c3.json 2> gpurun_out/r02_mle_c3.log
 tail -c 700 gpurun_out/r02_mle_c3.json; tail -2 gpurun_out/r02_mle_c3.log | cut -c1-300
