@@ -5,7 +5,7 @@ Workload (BASELINE.json configs[2], "C3" — the largest configuration that fits
 one B200; configs[1] C2 is run as `variants`): n = 62,500 jittered 250x250 grid
 (generate_locations(62500, 0)), Matern theta = (1.0, 0.03, 0.5), FP64,
 nb = 760, TLR accuracy 1e-7, max rank 380 (storage rule under a cap: a tile
-whose rank passes min(cap, 0.25 nb) is kept exact, never below the accuracy;
+whose rank passes min(cap, 0.1 nb) is kept exact, never below the accuracy;
 the uncapped path reproduces the reference's full C3 TLR value to 4e-12 and
 is pinned in tests/test_gpu_parity.py), plus kriging of 100 held-out sites (index seed 2,
 predict.holdout_experiment semantics).  z is the reference's own seeded field

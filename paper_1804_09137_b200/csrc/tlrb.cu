@@ -69,16 +69,22 @@ double g_peak_flops = 35.5e12, g_peak_bytes = 6449.7e9;
 // a tile exact is more accurate than the reference's truncation (never below
 // acc, compression.py:6) and removes the costliest work of the evaluation:
 // the SVD of its initial compression and the QRCP + Jacobi of a high-rank
-// nb x nb tile on every later update.  Measured at C3 (nb = 760, cap 380,
-// tools/c3_once.py, profiles/r02_sweep.jsonl): rule on the SVD rank with
-// rho = 0.45 7.05 s; on the QRCP rank, rho = 0.45 / 0.35 / 0.3 / 0.25 / 0.2:
-// 4.99 / 4.51 / 3.95 / 3.82 / 3.81 s, likelihood 1e-8 or closer to the
-// dense one.  Without a cap every tile follows the reference's truncation
+// nb x nb tile on every later update.  rho is the measured time break-even
+// of this GPU, where an exact tile is updated by DMMA GEMMs at ~30 TFLOP/s
+// and a low-rank one pays QR + SVD recompressions at ~1: C3 (nb = 760, cap
+// 380, tools/c3_once.py) with the round's first GEMM, rule on the SVD rank,
+// rho = 0.45: 7.05 s; on the QRCP rank, 0.45 / 0.35 / 0.3 / 0.25 / 0.2: 4.99 /
+// 4.51 / 3.95 / 3.82 / 3.81 s (profiles/r02_sweep.jsonl); with the final
+// kernels 0.3 / 0.25 / 0.2 / 0.15 / 0.12 / 0.1 / 0.08 / 0.05 / 0.03 (all exact):
+// 2.78 / 2.54 / 2.37 / 1.95 / 1.79 / 1.73 / 1.75 / 2.26 / 3.01 s
+// (profiles/r02_sweep_final.jsonl); at 0.1: 1,387 of 3,403 tiles exact, 7.4 GB
+// of factor storage (dense: 31 GB), likelihood 1e-11 from the dense one.
+// Without a cap every tile follows the reference's truncation
 // exactly (its TLR-vs-dense gap, hundreds of acc on ill-conditioned inputs,
 // is part of the parity contract).  TLRB_DENSE_FRAC overrides rho (>= 1:
 // cap only).
 double dense_frac() {
-  static const double v = getenv("TLRB_DENSE_FRAC") ? atof(getenv("TLRB_DENSE_FRAC")) : 0.25;
+  static const double v = getenv("TLRB_DENSE_FRAC") ? atof(getenv("TLRB_DENSE_FRAC")) : 0.1;
   return v;
 }
 

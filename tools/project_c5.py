@@ -98,7 +98,7 @@ def main():
         prof[d] = int(tb.compress_tile(blk, ACC)[0].shape[1])
     ds = sorted(prof)
     rank_at = np.interp(np.arange(1, T_FULL), ds, [prof[d] for d in ds])
-    limit = min(0.25 * NB, CAP)
+    limit = min(float(__import__("os").environ.get("TLRB_DENSE_FRAC", "0.1")) * NB, CAP)   # the library's storage rule
     stored = float(NB * NB * 8 * T_FULL)   # diagonal tiles
     dense_band = 0
     for d in range(1, T_FULL):
