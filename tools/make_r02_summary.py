@@ -32,6 +32,12 @@ print("\n## Counters per kernel class (`ncu --set full`, launches past the first
 _cnt = G / "r02_counters.md"
 reps = sorted(glob.glob(str(G / "r02_full_*.ncu-rep")))
 print(_cnt.read_text() if _cnt.exists() else run("tools/ncu_rep_table.py", *reps))
+_gb = ROOT / "profiles" / "r02_counters_gemmbench.md"
+if _gb.exists():
+    print("\nThe in-evaluation captures above land on small GEMM launches (look-ahead SYRK, K x K products); the "
+          "large-launch behaviour of the same kernel, `ncu --set full` on `tools/bench_gemm` (760 x 760 x 200 batch of 64, "
+          "82 x 760^3 batch, 4096^3):\n")
+    print(_gb.read_text())
 print("\nGEMM microbenchmark (`tools/bench_gemm`, ours vs cuBLAS on the TLR shapes): `profiles/r02_gemm_bench.txt`.\n")
 notes = ROOT / "profiles" / "r02_summary_notes.md"
 if notes.exists():
