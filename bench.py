@@ -234,6 +234,10 @@ def workload_config(cfg: str, world: int = 1) -> dict:
                       + (f" + kriging of {c['m']} held-out" if c.get("m") else "")),
          "n": c["n"], "nb": c["nb"], "acc": c["acc"], "max_rank": c["max_rank"] or None,
          "l2": "flushed before every step (256 MB write); tile working set > L2"}
+    if c["max_rank"]:
+        d["storage_rule"] = ("under the cap a tile whose rank passes min(max_rank, 0.1 nb) is kept exact (never below "
+                             "the accuracy); without a cap the reference's own truncation runs (C3: 19.0 s, 4e-12 from "
+                             "the reference's TLR value)")
     if world > 1:
         from paper_1804_09137_b200.dist import grid_shape
         p, q = grid_shape(world)
