@@ -559,7 +559,10 @@ __global__ void __launch_bounds__(512) bq_norms_kernel(const QrcpProb* __restric
   if (tid == 0) {
     const double stop = st[blockIdx.x].stop;
     const int kmax = min(P.m, P.n);
-    if (e <= stop || j + bb >= kmax) {
+    // (rank cap: once the steps taken exceed P.cap and the residual is still
+    // above the stop, the rank is known to exceed the cap -- all the caller
+    // asks; the reported rank j + bb > cap is a lower bound)
+    if (e <= stop || j + bb >= kmax || (P.cap > 0 && j + bb > P.cap)) {
       int s = j + bb;
       double res = e;
       for (int t = bb - 1; t >= 0; --t) {
@@ -585,7 +588,7 @@ void launch_qrcp_blocked(const std::vector<QrcpProb>& probs, DescArena& ar, cuda
   for (const QrcpProb& p : probs) {
     mmax = std::max(mmax, p.m);
     nmax = std::max(nmax, p.n);
-    hmax = std::max(hmax, p.hint);
+    hmax = std::max(hmax, p.cap > 0 ? std::min(p.hint, p.cap + 32) : p.hint);
   }
   // block width: the panel (mmax x b doubles) must fit in shared memory
   static const int b_env = getenv("TLRB_BQ_B") ? atoi(getenv("TLRB_BQ_B")) : 32;

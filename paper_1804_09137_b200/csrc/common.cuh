@@ -153,7 +153,9 @@ struct SumsqProb { const double* A; int ld, m, n; double* out; };
 struct CopyProb { const double* src; int lds; double* dst; int ldd; int m, n; int transpose; double scale;
                   int tri; const int* rowperm; const int* srccol = nullptr; };
 struct QrcpProb { double* A; int lda, m, n; int* perm; int* r_out; double* resid_out; double stop_rel2;
-                  int hint = 0; };   // hint: predicted number of QRCP steps (selects the kernel)
+                  int hint = 0;      // hint: predicted number of QRCP steps (selects the kernel)
+                  int cap = 0; };    // > 0: the caller only needs to know whether the rank exceeds cap (the tile is then
+                                     // stored exactly): the blocked QRCP stops at the first block past it
 
 // Device-resident descriptor staging (pinned host ring -> device), reset at
 // stream synchronisation points.

@@ -378,6 +378,9 @@ void compress_jobs(tlrb_handle* h, std::vector<Job>& jobs, double acc, int j0 = 
       cp.push_back({J.M, J.m, J.E, J.m, J.m, J.n, 0, 1.0, 0, nullptr});
       qp.push_back({J.M, J.m, J.m, J.n, d_perm + (size_t)j * h->nb, d_rank + j, d_sums + 6 * j + 1,
                     (qrcp_rel_tol() * acc) * (qrcp_rel_tol() * acc), J.s});
+      // a tile whose QRCP rank passes the dense limit is stored exactly: its QRCP may stop there
+      if (dense_by_qrcp() && !J.factored && J.tile >= 0 && h->max_rank > 0)
+        qp.back().cap = dense_rank_limit(h, J.m, J.n);
     }
     launch_copy(cp, h->ar, s);
     launch_qrcp(qp, gathered, h->ar, s);
